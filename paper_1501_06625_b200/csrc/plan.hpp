@@ -1,0 +1,267 @@
+// plan.hpp -- host-side compile_plan for the CUDA tracker.
+//
+// Turns the structural homotopy (g, f, gamma, k) into flat int32/double tables
+// the kernels walk:
+//  * monomial table: distinct supports of g and f, ordered by
+//    size DESCENDING so the longest reverse-mode chains start first; the
+//    value and partials of monomial q live in the monomial workspace at
+//    mono_out[q] + p*32 (p = 0 value, p = 1+k partial k): a warp's 32
+//    consecutive monomials write 32 consecutive entries per step (coalesced,
+//    the "aligned" layout of PAPER.md:434-442).
+//  * slot tasks: one per output entry (row i, col j), j == n is the value
+//    slot.  Each task carries the contribution lists of g and f in term order
+//    and the canonical-sum widths; equations identical in g and f are summed
+//    once ("shared").
+//  * contributions: (coefficient index, workspace index); workspace index -1
+//    marks a constant term whose contribution is the coefficient itself.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pathtrack_b200.h"
+
+namespace ptplan {
+
+constexpr int kWarpChunk = 32;
+
+inline int pow2ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+// Canonical widths; the oracle uses the same rules.
+inline int width_eval(int K) { return std::min(256, std::max(32, pow2ceil((K + 15) / 16))); }
+inline int width_mgs(int N) { return std::min(256, std::max(32, pow2ceil((N + 1) / 2))); }
+
+struct SlotTask {
+  int32_t row, col;
+  int32_t g_beg, g_cnt;
+  int32_t f_beg, f_cnt;  // f_cnt == -1: shared with g
+  int32_t gw;            // group width in warps = max canonical width / 32
+  int32_t pad;
+};
+
+struct HostPlan {
+  int n = 0, N = 0, L = 1;
+  // monomials (device order)
+  std::vector<int32_t> mono_size, mono_vbeg, mono_out, mono_flags, mono_var, mono_exp;
+  int64_t ws_len = 0;  // complex entries in the monomial workspace
+  // slots
+  std::vector<SlotTask> tasks;
+  int32_t class_beg[5] = {0, 0, 0, 0, 0};  // tasks with gw = 8,4,2,1
+  std::vector<int32_t> ctr_coef, ctr_ws;
+  // coefficients of all terms of g then f, complex SoA [2][L][n_coef]
+  std::vector<double> coef;
+  int64_t n_coef = 0;
+  int max_mono = 0;
+};
+
+inline void check(bool ok, const char* what) {
+  if (!ok) throw std::invalid_argument(what);
+}
+
+inline void validate(const pt_system_desc* s) {
+  check(s && s->eq_ptr && s->term_ptr && s->coef, "null system descriptor");
+  check(s->n_vars >= 1 && s->n_eqs >= 1 && s->n_terms >= 0, "bad system dimensions");
+  check(s->eq_ptr[0] == 0 && s->eq_ptr[s->n_eqs] == s->n_terms, "eq_ptr does not cover the terms");
+  for (int i = 0; i < s->n_eqs; ++i) check(s->eq_ptr[i] <= s->eq_ptr[i + 1], "eq_ptr not monotone");
+  check(s->term_ptr[0] == 0, "term_ptr[0] != 0");
+  for (int t = 0; t < s->n_terms; ++t) {
+    check(s->term_ptr[t] <= s->term_ptr[t + 1], "term_ptr not monotone");
+    for (int q = s->term_ptr[t]; q < s->term_ptr[t + 1]; ++q) {
+      check(s->var[q] >= 0 && s->var[q] < s->n_vars, "variable index out of range");
+      check(s->exp[q] >= 1, "exponent < 1");
+      if (q > s->term_ptr[t]) check(s->var[q] > s->var[q - 1], "support variables not strictly increasing");
+    }
+  }
+}
+
+inline HostPlan compile(const pt_system_desc* g, const pt_system_desc* f, int L) {
+  validate(g);
+  validate(f);
+  check(g->n_vars == f->n_vars && g->n_eqs == f->n_eqs, "start and target dimensions differ");
+  check(g->n_eqs >= g->n_vars, "need N >= n equations");
+  HostPlan P;
+  P.n = g->n_vars;
+  P.N = g->n_eqs;
+  P.L = L;
+  const int n = P.n, N = P.N;
+  const pt_system_desc* sys[2] = {g, f};
+
+  // --- distinct supports in first-appearance order ------------------------
+  using Key = std::vector<int32_t>;  // var0, exp0, var1, exp1, ...
+  std::map<Key, int> index;
+  std::vector<Key> keys;
+  std::vector<int> term_mono[2];
+  for (int s = 0; s < 2; ++s) {
+    const pt_system_desc* d = sys[s];
+    term_mono[s].resize(d->n_terms);
+    for (int t = 0; t < d->n_terms; ++t) {
+      Key k;
+      for (int q = d->term_ptr[t]; q < d->term_ptr[t + 1]; ++q) {
+        k.push_back(d->var[q]);
+        k.push_back(d->exp[q]);
+      }
+      if (k.empty()) {
+        term_mono[s][t] = -1;
+        continue;
+      }
+      auto it = index.find(k);
+      if (it == index.end()) {
+        it = index.emplace(k, (int)keys.size()).first;
+        keys.push_back(k);
+      }
+      term_mono[s][t] = it->second;
+    }
+  }
+  const int M = (int)keys.size();
+  // device order: size descending, ties by first appearance
+  std::vector<int> order(M);
+  for (int q = 0; q < M; ++q) order[q] = q;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return keys[a].size() > keys[b].size(); });
+  std::vector<int> dev_of(M);
+  for (int q = 0; q < M; ++q) dev_of[order[q]] = q;
+  P.mono_size.resize(M);
+  P.mono_vbeg.resize(M);
+  P.mono_out.resize(M);
+  P.mono_flags.resize(M);
+  // chunked workspace layout: chunk c = monomials [32c, 32c+32) uses
+  // 32 * (max size in chunk + 1) entries
+  int64_t ws = 0;
+  for (int c0 = 0; c0 < M; c0 += kWarpChunk) {
+    int maxsz = 0;
+    for (int q = c0; q < std::min(M, c0 + kWarpChunk); ++q) maxsz = std::max(maxsz, (int)keys[order[q]].size() / 2);
+    for (int q = c0; q < std::min(M, c0 + kWarpChunk); ++q) P.mono_out[q] = (int32_t)(ws + (q - c0));
+    ws += (int64_t)kWarpChunk * (maxsz + 1);
+  }
+  check(ws < (int64_t)1 << 31, "monomial workspace exceeds 2^31 entries");
+  P.ws_len = std::max<int64_t>(ws, 1);
+  for (int q = 0; q < M; ++q) {
+    const Key& k = keys[order[q]];
+    const int m = (int)k.size() / 2;
+    P.mono_size[q] = m;
+    P.mono_vbeg[q] = (int32_t)P.mono_var.size();
+    int flags = 0;
+    for (int p = 0; p < m; ++p) {
+      P.mono_var.push_back(k[2 * p]);
+      P.mono_exp.push_back(k[2 * p + 1]);
+      if (k[2 * p + 1] >= 2) flags |= 1;
+    }
+    P.mono_flags[q] = flags;
+    P.max_mono = std::max(P.max_mono, m);
+  }
+  if (P.mono_var.empty()) {
+    P.mono_var.push_back(0);
+    P.mono_exp.push_back(1);
+  }
+
+  // --- coefficients: g terms then f terms ---------------------------------
+  P.n_coef = (int64_t)g->n_terms + f->n_terms;
+  const int64_t NC = std::max<int64_t>(P.n_coef, 1);
+  P.coef.assign((size_t)2 * L * NC, 0.0);
+  for (int s = 0; s < 2; ++s) {
+    const pt_system_desc* d = sys[s];
+    const int64_t base = s == 0 ? 0 : g->n_terms;
+    for (int t = 0; t < d->n_terms; ++t)
+      for (int q = 0; q < 2 * L; ++q) P.coef[(size_t)q * NC + base + t] = d->coef[(size_t)q * d->n_terms + t];
+  }
+  P.n_coef = NC;
+
+  // --- shared equations ----------------------------------------------------
+  std::vector<char> shared(N, 0);
+  for (int i = 0; i < N; ++i) {
+    const int gb = g->eq_ptr[i], ge = g->eq_ptr[i + 1], fb = f->eq_ptr[i], fe = f->eq_ptr[i + 1];
+    bool same = (ge - gb) == (fe - fb);
+    for (int q = 0; same && q < ge - gb; ++q) {
+      same = term_mono[0][gb + q] == term_mono[1][fb + q];
+      for (int l = 0; same && l < 2 * L; ++l) {
+        const double a = g->coef[(size_t)l * g->n_terms + gb + q];
+        const double b = f->coef[(size_t)l * f->n_terms + fb + q];
+        same = std::memcmp(&a, &b, 8) == 0;
+      }
+    }
+    shared[i] = same;
+  }
+
+  // --- slot contribution lists --------------------------------------------
+  // per system, per equation: value list + per-variable lists, in term order
+  struct Lists {
+    std::vector<int32_t> coef, wsi;
+  };
+  std::vector<SlotTask> tasks;
+  tasks.reserve((size_t)N * (n + 1));
+  std::vector<std::vector<Lists>> L2(2, std::vector<Lists>(n + 1));
+  for (int i = 0; i < N; ++i) {
+    const int ns = shared[i] ? 1 : 2;
+    for (int s = 0; s < ns; ++s) {
+      for (auto& l : L2[s]) {
+        l.coef.clear();
+        l.wsi.clear();
+      }
+      const pt_system_desc* d = sys[s];
+      const int64_t cbase = s == 0 ? 0 : g->n_terms;
+      for (int t = d->eq_ptr[i]; t < d->eq_ptr[i + 1]; ++t) {
+        const int mo = term_mono[s][t];
+        const int32_t ci = (int32_t)(cbase + t);
+        if (mo < 0) {
+          L2[s][n].coef.push_back(ci);
+          L2[s][n].wsi.push_back(-1);
+          continue;
+        }
+        const int q = dev_of[mo];
+        L2[s][n].coef.push_back(ci);
+        L2[s][n].wsi.push_back(P.mono_out[q]);
+        for (int p = d->term_ptr[t]; p < d->term_ptr[t + 1]; ++p) {
+          const int k = p - d->term_ptr[t];
+          L2[s][d->var[p]].coef.push_back(ci);
+          L2[s][d->var[p]].wsi.push_back(P.mono_out[q] + kWarpChunk * (1 + k));
+        }
+      }
+    }
+    for (int j = 0; j <= n; ++j) {
+      SlotTask tk{};
+      tk.row = i;
+      tk.col = j;
+      tk.g_beg = (int32_t)P.ctr_coef.size();
+      tk.g_cnt = (int32_t)L2[0][j].coef.size();
+      P.ctr_coef.insert(P.ctr_coef.end(), L2[0][j].coef.begin(), L2[0][j].coef.end());
+      P.ctr_ws.insert(P.ctr_ws.end(), L2[0][j].wsi.begin(), L2[0][j].wsi.end());
+      int w = tk.g_cnt > 0 ? width_eval(tk.g_cnt) : 32;
+      if (shared[i]) {
+        tk.f_beg = tk.g_beg;
+        tk.f_cnt = -1;
+      } else {
+        tk.f_beg = (int32_t)P.ctr_coef.size();
+        tk.f_cnt = (int32_t)L2[1][j].coef.size();
+        P.ctr_coef.insert(P.ctr_coef.end(), L2[1][j].coef.begin(), L2[1][j].coef.end());
+        P.ctr_ws.insert(P.ctr_ws.end(), L2[1][j].wsi.begin(), L2[1][j].wsi.end());
+        if (tk.f_cnt > 0) w = std::max(w, width_eval(tk.f_cnt));
+      }
+      check(P.ctr_coef.size() < ((size_t)1 << 31), "too many contributions");
+      tk.gw = w / 32;
+      tasks.push_back(tk);
+    }
+  }
+  // group tasks by width class (8, 4, 2, 1 warps); stable within a class
+  const int classes[4] = {8, 4, 2, 1};
+  for (int c = 0; c < 4; ++c) {
+    P.class_beg[c] = (int32_t)P.tasks.size();
+    for (auto& tk : tasks)
+      if (tk.gw == classes[c]) P.tasks.push_back(tk);
+  }
+  P.class_beg[4] = (int32_t)P.tasks.size();
+  if (P.ctr_coef.empty()) {
+    P.ctr_coef.push_back(0);
+    P.ctr_ws.push_back(-1);
+  }
+  return P;
+}
+
+}  // namespace ptplan

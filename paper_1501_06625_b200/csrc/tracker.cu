@@ -1,0 +1,762 @@
+// tracker.cu -- kernels and the C-ABI (include/pathtrack_b200.h).
+//
+//   k_track_grid<R>   one path, cooperative persistent grid (GridTeam)
+//   k_track_batch<R>  many paths, one CTA per path, atomic path queue
+//   k_eval<R>         evaluate_homotopy only (parity tests)
+//   k_lstsq<R>        least_squares_solve only (parity tests)
+//   k_arith<R>        bulk scalar ops (arithmetic parity tests)
+// There is no host fallback: every compute entry point needs an sm_100 device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+
+using namespace ptdev;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define PT_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) return fail(PT_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline int limbs(pt_prec p) { return p == PT_D ? 1 : (p == PT_DD ? 2 : 4); }
+
+// Per-path workspace layout (element counts); slice b of a batch starts at
+// b * dslice doubles / b * uslice u64 words.
+struct Layout {
+  long x, hist, ws, A, Rm, inv, rmaxp, hmod, scal, dx;  // double offsets
+  long dslice;
+  long flags, ctl;  // u64 offsets
+  long uslice;
+};
+
+Layout make_layout(int L, int n, int N, long ws_len) {
+  Layout o{};
+  long d = 0;
+  auto take = [&](long cnt) {
+    long at = d;
+    d += (cnt + 31) & ~31L;  // 256-byte aligned sub-arrays
+    return at;
+  };
+  o.x = take(2L * L * n);
+  o.hist = take((long)(kMaxDegree + 1) * 2 * L * n);
+  o.ws = take(2L * L * ws_len);
+  o.A = take(2L * L * N * (n + 1));
+  o.Rm = take(2L * L * n * (n + 1));
+  o.inv = take((long)L * n);
+  o.rmaxp = take(n);
+  o.hmod = take(N);
+  o.scal = take(8);
+  o.dx = take(2L * L * n);
+  o.dslice = d;
+  long u = 0;
+  o.flags = u;
+  u += (n + 1 + 31) & ~31L;
+  o.ctl = u;
+  u += 32;
+  o.uslice = u;
+  return o;
+}
+
+__host__ __device__ inline Work carve(double* dbase, unsigned long long* ubase, const Layout& o, long b) {
+  double* d = dbase + b * o.dslice;
+  unsigned long long* u = ubase + b * o.uslice;
+  Work W;
+  W.x = d + o.x;
+  W.hist = d + o.hist;
+  W.ws = d + o.ws;
+  W.A = d + o.A;
+  W.Rm = d + o.Rm;
+  W.inv = d + o.inv;
+  W.rmaxp = d + o.rmaxp;
+  W.hmod = d + o.hmod;
+  W.scal = d + o.scal;
+  W.dx = d + o.dx;
+  W.flags = u + o.flags;
+  W.ctl = u + o.ctl;
+  return W;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+template <class R>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_track_grid(DevPlan P, Work W, pt_step_params sp, TrackIO io, unsigned long long epoch_base) {
+  __shared__ Smem<R> sh;
+  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x};
+  track_path<R, GridTeam>(P, W, team, sh, sp, io, epoch_base);
+}
+
+template <class R>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_track_batch(DevPlan P, double* dbase, unsigned long long* ubase, Layout lay, pt_step_params sp,
+                  const double* starts, double* ends, pt_path_stats* stats, int n_paths,
+                  unsigned long long* queue, unsigned long long epoch_base) {
+  __shared__ Smem<R> sh;
+  __shared__ int s_path;
+  const Work W = carve(dbase, ubase, lay, blockIdx.x);
+  const BlockTeam team{W.ctl, 1, 0};
+  const long PS = 2L * limbs_of<R>::L * P.n;
+  for (;;) {
+    if (threadIdx.x == 0) s_path = (int)atomicAdd(queue, 1ull);
+    __syncthreads();
+    const int p = s_path;
+    __syncthreads();
+    if (p >= n_paths) break;
+    TrackIO io{starts + p * PS, ends + p * PS, stats + p, nullptr, 0, nullptr};
+    track_path<R, BlockTeam>(P, W, team, sh, sp, io, epoch_base + ((unsigned long long)p << 16));
+  }
+}
+
+template <class R>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_eval(DevPlan P, Work W, const double* x, double t, double* h, double* J, double* rmax) {
+  __shared__ Smem<R> sh;
+  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x};
+  const int n = P.n, N = P.N;
+  if (team.block == 0)
+    for (int i = threadIdx.x; i < n; i += kThreads) store_c<R>(W.x, n, i, load_c<R>(x, n, i));
+  if (!team.sync(&sh.flag)) return;
+  eval_monomials<R>(P, W, team.block * kThreads + threadIdx.x, team.nblocks * kThreads);
+  if (!team.sync(&sh.flag)) return;
+  eval_slots<R, GridTeam>(P, W, team, sh, t);
+  if (!team.sync(&sh.flag)) return;
+  const long SA = (long)N * (n + 1), SJ = (long)N * n;
+  const long tid = (long)team.block * kThreads + threadIdx.x, nth = (long)team.nblocks * kThreads;
+  if (J)
+    for (long q = tid; q < SJ; q += nth) store_c<R>(J, SJ, q, load_c<R>(W.A, SA, q));
+  if (h)
+    for (long i = tid; i < N; i += nth) store_c<R>(h, N, i, c_neg(load_c<R>(W.A, SA, (long)n * N + i)));
+  if (team.block == 0) {
+    double r = 0.0;
+    for (int i = threadIdx.x; i < N; i += kThreads) r = nan_max(r, W.hmod[i]);
+    r = block_nan_max(r, sh.red);
+    if (threadIdx.x == 0 && rmax) *rmax = r;
+  }
+}
+
+template <class R>
+__global__ void __launch_bounds__(kThreads, 1) k_lstsq(DevPlan P, Work W, unsigned long long epoch, int* status) {
+  __shared__ Smem<R> sh;
+  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x};
+  mgs<R, GridTeam>(P, W, team, sh, epoch, kSqrtEps<R>());
+  if (!team.sync(&sh.flag)) {
+    if (team.block == 0 && threadIdx.x == 0) *status = PT_E_TIMEOUT;
+    return;
+  }
+  if (ld_acquire(W.ctl + CTL_RANK) == epoch) {
+    if (team.block == 0 && threadIdx.x == 0) *status = PT_E_RANK;
+    return;
+  }
+  if (team.block == 0) {
+    backsub_update<R>(P, W, sh);
+    if (threadIdx.x == 0) *status = 0;
+  }
+}
+
+template <class R>
+__device__ R arith_rd(const double* p) {
+  R v;
+#pragma unroll
+  for (int l = 0; l < limbs_of<R>::L; ++l) r_set_limb(v, l, p[l]);
+  return v;
+}
+template <class R>
+__host__ __device__ inline void arith_one(int op, const double* pa, const double* pb, double* po) {
+  constexpr int L = limbs_of<R>::L;
+  auto rd = [](const double* p) {
+    R v;
+    for (int l = 0; l < L; ++l) r_set_limb(v, l, p[l]);
+    return v;
+  };
+  auto wr = [](const R& v, double* p) {
+    for (int l = 0; l < L; ++l) p[l] = r_limb(v, l);
+  };
+  const R ar = rd(pa), br = rd(pb);
+  const cplx<R> ac{rd(pa), rd(pa + L)}, bc{rd(pb), rd(pb + L)};
+  cplx<R> oc;
+  switch (op) {
+    case 0: wr(r_add(ar, br), po); break;
+    case 1: wr(r_sub(ar, br), po); break;
+    case 2: wr(r_mul(ar, br), po); break;
+    case 3: wr(r_mul_d(ar, pb[0]), po); break;
+    case 4: wr(r_div(ar, br), po); break;
+    case 5: wr(r_sqrt(ar), po); break;
+    case 6:
+      if constexpr (L == 4) {
+        wr(qd_renormalize(ar), po);
+      } else if constexpr (L == 2) {
+        wr(dd_norm(r_limb(ar, 0), r_limb(ar, 1)), po);
+      } else {
+        wr(ar, po);
+      }
+      break;
+    case 7: oc = c_mul(ac, bc); wr(oc.re, po); wr(oc.im, po + L); break;
+    case 8: oc = c_add(ac, bc); wr(oc.re, po); wr(oc.im, po + L); break;
+    case 9: oc = c_conj_mul(ac, bc); wr(oc.re, po); wr(oc.im, po + L); break;
+    case 10: wr(c_norm_sqr(ac), po); break;
+    case 11: po[0] = c_mod_double(ac); break;
+    case 12: wr(r_powi(ar, (unsigned)pb[0]), po); break;
+    case 14: oc = c_scale(ac, br); wr(oc.re, po); wr(oc.im, po + L); break;
+    case 15: oc = c_powi(ac, (unsigned)pb[0]); wr(oc.re, po); wr(oc.im, po + L); break;
+    default: break;
+  }
+}
+
+template <class R>
+__global__ void k_arith(int op, long count, const double* a, const double* b, double* out) {
+  constexpr int L = limbs_of<R>::L;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    arith_one<R>(op, a + i * 2 * L, b + i * 2 * L, out + i * 2 * L);
+}
+
+// ---------------------------------------------------------------------------
+// plan object
+// ---------------------------------------------------------------------------
+struct pt_plan {
+  int device = 0;
+  pt_prec prec = PT_DD;
+  int L = 2;
+  int n = 0, N = 0, M = 0;
+  long n_ctr = 0;
+  cudaStream_t stream = nullptr;
+  DevPlan dp{};
+  Layout lay{};
+  void* dtables = nullptr;  // plan tables
+  double* dwork = nullptr;  // single-path workspace (slice 0)
+  unsigned long long* uwork = nullptr;
+  int grid_blocks = 1;
+  // staging for the host-buffer API
+  double* d_start = nullptr;
+  double* d_end = nullptr;
+  pt_path_stats* d_stats = nullptr;
+  pt_trace_event* d_trace = nullptr;
+  int* d_trace_len = nullptr;
+  int trace_cap = 0;
+  // batch
+  double* bwork = nullptr;
+  unsigned long long* bu = nullptr;
+  int batch_blocks = 0;
+  unsigned long long* d_queue = nullptr;
+  double* b_starts = nullptr;
+  double* b_ends = nullptr;
+  pt_path_stats* b_stats = nullptr;
+  long b_cap = 0;
+  unsigned long long launches = 0;
+};
+
+namespace {
+
+template <class R>
+const void* grid_kernel() {
+  return reinterpret_cast<const void*>(&k_track_grid<R>);
+}
+
+int occupancy_blocks(const void* fn, int device, int* per_sm, int* sms) {
+  cudaDeviceProp prop;
+  PT_CUDA(cudaGetDeviceProperties(&prop, device));
+  *sms = prop.multiProcessorCount;
+  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, kThreads, 0));
+  return PT_OK;
+}
+
+int check_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return fail(PT_E_NODEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+  if (device < 0 || device >= count) return fail(PT_E_NODEVICE, "device index out of range");
+  cudaDeviceProp prop;
+  PT_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) return fail(PT_E_NODEVICE, "device is not sm_100 class");
+  return PT_OK;
+}
+
+template <class R>
+int dispatch_grid_size(pt_plan* p, const void* fn) {
+  int per_sm = 0, sms = 0;
+  int rc = occupancy_blocks(fn, p->device, &per_sm, &sms);
+  if (rc) return rc;
+  const int cap = std::max(1, per_sm) * sms;
+  // enough CTAs that each phase has about one unit of work per warp / group
+  const long ntasks = p->dp.class_beg[4];
+  const int gpc_mgs = kWarps / (p->dp.P_mgs / 32);
+  long want = 1;
+  want = std::max(want, (long)(p->M + kThreads - 1) / kThreads);
+  want = std::max(want, (ntasks + kWarps - 1) / kWarps);
+  want = std::max(want, (long)(p->n + 1 + gpc_mgs - 1) / gpc_mgs);
+  p->grid_blocks = (int)std::min<long>(want, std::min(cap, sms));
+  return PT_OK;
+}
+
+template <class T>
+T* dev_alloc(size_t count, int* rc) {
+  T* ptr = nullptr;
+  cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    *rc = fail(PT_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return nullptr;
+  }
+  return ptr;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    return fail(PT_E_INVAL, e.what());
+  }
+}
+
+template <class R>
+void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
+  Work W = carve(p->dwork, p->uwork, p->lay, 0);
+  unsigned long long epoch = (++p->launches) << 40;
+  DevPlan dp = p->dp;
+  pt_step_params spc = sp;
+  TrackIO ioc = io;
+  void* args[] = {&dp, &W, &spc, &ioc, &epoch};
+  *err = cudaLaunchCooperativeKernel((const void*)&k_track_grid<R>, dim3(p->grid_blocks), dim3(kThreads), args, 0, s);
+}
+
+int validate_params(const pt_step_params* sp) {
+  if (!sp) return fail(PT_E_INVAL, "null step params");
+  if (sp->pred_degree < 0 || sp->pred_degree > kMaxDegree) return fail(PT_E_INVAL, "pred_degree must be 0..8");
+  if (sp->newton_max_iter < 1) return fail(PT_E_INVAL, "newton_max_iter must be >= 1");
+  if (!(sp->min_step > 0.0) || !(sp->max_step >= sp->min_step) || !(sp->max_step <= 1.0))
+    return fail(PT_E_INVAL, "need 0 < min_step <= max_step <= 1");
+  if (sp->max_steps < 0) return fail(PT_E_INVAL, "max_steps must be >= 0");
+  return PT_OK;
+}
+
+int read_abort(pt_plan* p, unsigned long long* ctl) {
+  unsigned long long h[CTL_WORDS];
+  PT_CUDA(cudaMemcpy(h, ctl, sizeof h, cudaMemcpyDeviceToHost));
+  if (h[CTL_ABORT]) {
+    // reset barrier state so the plan stays usable
+    PT_CUDA(cudaMemset(ctl, 0, sizeof h));
+    return fail(PT_E_TIMEOUT, "device watchdog fired (grid barrier or MGS flag stalled)");
+  }
+  return PT_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* pt_last_error(void) { return g_err.c_str(); }
+const char* pt_version(void) { return "pathtrack_b200 0.1 (sm_100a)"; }
+
+int pt_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int pt_default_params(pt_prec prec, pt_step_params* out) {
+  if (!out) return PT_E_INVAL;
+  out->max_step = 0.1;
+  out->min_step = 1e-6;
+  out->max_steps = prec == PT_QD ? 1500 : 500;
+  out->pred_degree = 4;
+  out->newton_max_iter = 6;
+  out->reserved = 0;
+  out->newton_tol = prec == PT_D ? 1e-8 : (prec == PT_DD ? 1e-20 : 1e-44);
+  return PT_OK;
+}
+
+int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_system_desc* f,
+                   const double* gamma, int32_t relax_k, pt_plan** out) {
+  return guarded([&]() -> int {
+    if (!out || !gamma || relax_k < 1) return fail(PT_E_INVAL, "bad plan arguments");
+    if (prec != PT_D && prec != PT_DD && prec != PT_QD) return fail(PT_E_INVAL, "bad precision");
+    int rc = check_device(device);
+    if (rc) return rc;
+    const int L = limbs(prec);
+    ptplan::HostPlan hp = ptplan::compile(g, f, L);
+    if (hp.n > kMaxRowsPerThread * kThreads) return fail(PT_E_INVAL, "n_vars > 1024 not supported");
+    PT_CUDA(cudaSetDevice(device));
+    auto p = std::make_unique<pt_plan>();
+    p->device = device;
+    p->prec = prec;
+    p->L = L;
+    p->n = hp.n;
+    p->N = hp.N;
+    p->M = (int)hp.mono_size.size();
+    p->n_ctr = (long)hp.ctr_coef.size();
+    PT_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    // tables: one allocation, 256-byte aligned pieces
+    std::vector<std::pair<const void*, size_t>> pieces = {
+        {hp.mono_size.data(), hp.mono_size.size() * 4}, {hp.mono_vbeg.data(), hp.mono_vbeg.size() * 4},
+        {hp.mono_out.data(), hp.mono_out.size() * 4},   {hp.mono_flags.data(), hp.mono_flags.size() * 4},
+        {hp.mono_var.data(), hp.mono_var.size() * 4},   {hp.mono_exp.data(), hp.mono_exp.size() * 4},
+        {hp.tasks.data(), hp.tasks.size() * sizeof(ptplan::SlotTask)},
+        {hp.ctr_coef.data(), hp.ctr_coef.size() * 4},   {hp.ctr_ws.data(), hp.ctr_ws.size() * 4},
+        {hp.coef.data(), hp.coef.size() * 8},           {gamma, (size_t)2 * L * 8}};
+    size_t total = 0;
+    std::vector<size_t> offs;
+    for (auto& pc : pieces) {
+      offs.push_back(total);
+      total += (pc.second + 255) & ~(size_t)255;
+    }
+    rc = 0;
+    char* base = dev_alloc<char>(total, &rc);
+    if (rc) return rc;
+    p->dtables = base;
+    for (size_t q = 0; q < pieces.size(); ++q)
+      if (pieces[q].second) PT_CUDA(cudaMemcpy(base + offs[q], pieces[q].first, pieces[q].second, cudaMemcpyHostToDevice));
+    DevPlan& dp = p->dp;
+    dp.n = hp.n;
+    dp.N = hp.N;
+    dp.M = p->M;
+    dp.P_mgs = ptplan::width_mgs(hp.N);
+    dp.mono_size = (const int32_t*)(base + offs[0]);
+    dp.mono_vbeg = (const int32_t*)(base + offs[1]);
+    dp.mono_out = (const int32_t*)(base + offs[2]);
+    dp.mono_flags = (const int32_t*)(base + offs[3]);
+    dp.mono_var = (const int32_t*)(base + offs[4]);
+    dp.mono_exp = (const int32_t*)(base + offs[5]);
+    dp.ws_len = hp.ws_len;
+    dp.tasks = (const ptplan::SlotTask*)(base + offs[6]);
+    for (int c = 0; c < 5; ++c) dp.class_beg[c] = hp.class_beg[c];
+    dp.ctr_coef = (const int32_t*)(base + offs[7]);
+    dp.ctr_ws = (const int32_t*)(base + offs[8]);
+    dp.coef = (const double*)(base + offs[9]);
+    dp.n_coef = hp.n_coef;
+    dp.gamma = (const double*)(base + offs[10]);
+    dp.relax_k = relax_k;
+    // single-path workspace
+    p->lay = make_layout(L, hp.n, hp.N, hp.ws_len);
+    p->dwork = dev_alloc<double>(p->lay.dslice, &rc);
+    if (rc) return rc;
+    p->uwork = dev_alloc<unsigned long long>(p->lay.uslice, &rc);
+    if (rc) return rc;
+    PT_CUDA(cudaMemset(p->dwork, 0, p->lay.dslice * 8));
+    PT_CUDA(cudaMemset(p->uwork, 0, p->lay.uslice * 8));
+    const size_t vec = (size_t)2 * L * hp.n;
+    p->d_start = dev_alloc<double>(vec, &rc);
+    if (rc) return rc;
+    p->d_end = dev_alloc<double>(vec, &rc);
+    if (rc) return rc;
+    p->d_stats = dev_alloc<pt_path_stats>(1, &rc);
+    if (rc) return rc;
+    p->d_trace_len = dev_alloc<int>(1, &rc);
+    if (rc) return rc;
+    switch (prec) {
+      case PT_D: rc = dispatch_grid_size<double>(p.get(), grid_kernel<double>()); break;
+      case PT_DD: rc = dispatch_grid_size<dd>(p.get(), grid_kernel<dd>()); break;
+      default: rc = dispatch_grid_size<qd>(p.get(), grid_kernel<qd>()); break;
+    }
+    if (rc) return rc;
+    *out = p.release();
+    return PT_OK;
+  });
+}
+
+void pt_plan_destroy(pt_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  for (void* q : {(void*)p->dtables, (void*)p->dwork, (void*)p->uwork, (void*)p->d_start, (void*)p->d_end,
+                  (void*)p->d_stats, (void*)p->d_trace, (void*)p->d_trace_len, (void*)p->bwork, (void*)p->bu,
+                  (void*)p->d_queue, (void*)p->b_starts, (void*)p->b_ends, (void*)p->b_stats})
+    if (q) cudaFree(q);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+int64_t pt_plan_info(const pt_plan* p, int32_t what) {
+  if (!p) return -1;
+  switch (what) {
+    case 0: return p->n;
+    case 1: return p->N;
+    case 2: return p->M;
+    case 3: return p->n_ctr;
+    case 4: return p->grid_blocks;
+    case 5: return p->prec;
+    case 6: return p->batch_blocks;
+    case 7: return p->dp.ws_len;
+  }
+  return -1;
+}
+
+int pt_plan_set_trace(pt_plan* p, int32_t capacity) {
+  if (!p || capacity < 0) return PT_E_INVAL;
+  PT_CUDA(cudaSetDevice(p->device));
+  if (p->d_trace) cudaFree(p->d_trace);
+  p->d_trace = nullptr;
+  p->trace_cap = 0;
+  if (capacity > 0) {
+    int rc = 0;
+    p->d_trace = dev_alloc<pt_trace_event>(capacity, &rc);
+    if (rc) return rc;
+    p->trace_cap = capacity;
+  }
+  return PT_OK;
+}
+
+int pt_plan_get_trace(pt_plan* p, pt_trace_event* out, int32_t capacity, int32_t* count) {
+  if (!p || !count) return PT_E_INVAL;
+  PT_CUDA(cudaSetDevice(p->device));
+  int len = 0;
+  PT_CUDA(cudaMemcpy(&len, p->d_trace_len, sizeof(int), cudaMemcpyDeviceToHost));
+  *count = len;
+  const int m = std::min({len, capacity, p->trace_cap});
+  if (m > 0 && out) PT_CUDA(cudaMemcpy(out, p->d_trace, m * sizeof(pt_trace_event), cudaMemcpyDeviceToHost));
+  return PT_OK;
+}
+
+int pt_track_path_device(pt_plan* p, const double* d_start, const pt_step_params* sp, double* d_end,
+                         pt_path_stats* d_stats, void* stream) {
+  if (!p || !d_start || !d_end || !d_stats) return fail(PT_E_INVAL, "null argument");
+  int rc = validate_params(sp);
+  if (rc) return rc;
+  PT_CUDA(cudaSetDevice(p->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
+  TrackIO io{d_start, d_end, d_stats, p->d_trace, p->trace_cap, p->d_trace_len};
+  cudaError_t err = cudaSuccess;
+  switch (p->prec) {
+    case PT_D: launch_grid<double>(p, *sp, io, s, &err); break;
+    case PT_DD: launch_grid<dd>(p, *sp, io, s, &err); break;
+    default: launch_grid<qd>(p, *sp, io, s, &err); break;
+  }
+  if (err != cudaSuccess) return fail(PT_E_CUDA, std::string("track launch: ") + cudaGetErrorString(err));
+  return PT_OK;
+}
+
+int pt_track_path(pt_plan* p, const double* start, const pt_step_params* sp, double* end, pt_path_stats* stats) {
+  if (!p || !start || !end || !stats) return fail(PT_E_INVAL, "null argument");
+  PT_CUDA(cudaSetDevice(p->device));
+  const size_t bytes = (size_t)2 * p->L * p->n * sizeof(double);
+  PT_CUDA(cudaMemcpyAsync(p->d_start, start, bytes, cudaMemcpyHostToDevice, p->stream));
+  int rc = pt_track_path_device(p, p->d_start, sp, p->d_end, p->d_stats, p->stream);
+  if (rc) return rc;
+  PT_CUDA(cudaMemcpyAsync(end, p->d_end, bytes, cudaMemcpyDeviceToHost, p->stream));
+  PT_CUDA(cudaMemcpyAsync(stats, p->d_stats, sizeof(pt_path_stats), cudaMemcpyDeviceToHost, p->stream));
+  PT_CUDA(cudaStreamSynchronize(p->stream));
+  return read_abort(p, carve(p->dwork, p->uwork, p->lay, 0).ctl);
+}
+
+static int ensure_batch(pt_plan* p) {
+  if (p->bwork) return PT_OK;
+  int per_sm = 0, sms = 0;
+  const void* fn = p->prec == PT_D    ? (const void*)&k_track_batch<double>
+                   : p->prec == PT_DD ? (const void*)&k_track_batch<dd>
+                                      : (const void*)&k_track_batch<qd>;
+  int rc = occupancy_blocks(fn, p->device, &per_sm, &sms);
+  if (rc) return rc;
+  p->batch_blocks = std::max(1, per_sm) * sms;
+  p->bwork = dev_alloc<double>((size_t)p->lay.dslice * p->batch_blocks, &rc);
+  if (rc) return rc;
+  p->bu = dev_alloc<unsigned long long>((size_t)p->lay.uslice * p->batch_blocks, &rc);
+  if (rc) return rc;
+  p->d_queue = dev_alloc<unsigned long long>(1, &rc);
+  if (rc) return rc;
+  PT_CUDA(cudaMemset(p->bwork, 0, (size_t)p->lay.dslice * p->batch_blocks * 8));
+  PT_CUDA(cudaMemset(p->bu, 0, (size_t)p->lay.uslice * p->batch_blocks * 8));
+  return PT_OK;
+}
+
+int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, const pt_step_params* sp,
+                          double* d_ends, pt_path_stats* d_stats, void* stream) {
+  if (!p || n_paths < 0 || (n_paths > 0 && (!d_starts || !d_ends || !d_stats))) return fail(PT_E_INVAL, "bad batch args");
+  int rc = validate_params(sp);
+  if (rc) return rc;
+  if (n_paths == 0) return PT_OK;
+  PT_CUDA(cudaSetDevice(p->device));
+  rc = ensure_batch(p);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
+  PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 8, s));
+  const unsigned long long epoch = (++p->launches) << 40;
+  const int blocks = std::min(p->batch_blocks, n_paths);
+  switch (p->prec) {
+    case PT_D:
+      k_track_batch<double><<<blocks, kThreads, 0, s>>>(p->dp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
+                                                        n_paths, p->d_queue, epoch);
+      break;
+    case PT_DD:
+      k_track_batch<dd><<<blocks, kThreads, 0, s>>>(p->dp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
+                                                    n_paths, p->d_queue, epoch);
+      break;
+    default:
+      k_track_batch<qd><<<blocks, kThreads, 0, s>>>(p->dp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
+                                                    n_paths, p->d_queue, epoch);
+      break;
+  }
+  PT_CUDA(cudaGetLastError());
+  return PT_OK;
+}
+
+int pt_track_batch(pt_plan* p, int32_t n_paths, const double* starts, const pt_step_params* sp, double* ends,
+                   pt_path_stats* stats) {
+  if (!p || n_paths < 0) return fail(PT_E_INVAL, "bad batch args");
+  if (n_paths == 0) return PT_OK;
+  PT_CUDA(cudaSetDevice(p->device));
+  const size_t vec = (size_t)2 * p->L * p->n;
+  if (p->b_cap < n_paths) {
+    for (void* q : {(void*)p->b_starts, (void*)p->b_ends, (void*)p->b_stats})
+      if (q) cudaFree(q);
+    int rc = 0;
+    p->b_starts = dev_alloc<double>(vec * n_paths, &rc);
+    if (rc) return rc;
+    p->b_ends = dev_alloc<double>(vec * n_paths, &rc);
+    if (rc) return rc;
+    p->b_stats = dev_alloc<pt_path_stats>(n_paths, &rc);
+    if (rc) return rc;
+    p->b_cap = n_paths;
+  }
+  PT_CUDA(cudaMemcpyAsync(p->b_starts, starts, vec * n_paths * 8, cudaMemcpyHostToDevice, p->stream));
+  int rc = pt_track_batch_device(p, n_paths, p->b_starts, sp, p->b_ends, p->b_stats, p->stream);
+  if (rc) return rc;
+  PT_CUDA(cudaMemcpyAsync(ends, p->b_ends, vec * n_paths * 8, cudaMemcpyDeviceToHost, p->stream));
+  PT_CUDA(cudaMemcpyAsync(stats, p->b_stats, sizeof(pt_path_stats) * n_paths, cudaMemcpyDeviceToHost, p->stream));
+  PT_CUDA(cudaStreamSynchronize(p->stream));
+  return PT_OK;
+}
+
+int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J, double* rmax) {
+  if (!p || !x) return fail(PT_E_INVAL, "null argument");
+  PT_CUDA(cudaSetDevice(p->device));
+  const int L = p->L, n = p->n, N = p->N;
+  int rc = 0;
+  double* dx = dev_alloc<double>((size_t)2 * L * n, &rc);
+  if (rc) return rc;
+  double* dh = dev_alloc<double>((size_t)2 * L * N, &rc);
+  double* dJ = dev_alloc<double>((size_t)2 * L * N * n, &rc);
+  double* dr = dev_alloc<double>(1, &rc);
+  if (rc) return rc;
+  PT_CUDA(cudaMemcpy(dx, x, (size_t)2 * L * n * 8, cudaMemcpyHostToDevice));
+  Work W = carve(p->dwork, p->uwork, p->lay, 0);
+  DevPlan dp = p->dp;
+  void* args[] = {&dp, &W, &dx, &t, &dh, &dJ, &dr};
+  const void* fn = p->prec == PT_D ? (const void*)&k_eval<double> : p->prec == PT_DD ? (const void*)&k_eval<dd> : (const void*)&k_eval<qd>;
+  PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, 0, p->stream));
+  PT_CUDA(cudaStreamSynchronize(p->stream));
+  if (h) PT_CUDA(cudaMemcpy(h, dh, (size_t)2 * L * N * 8, cudaMemcpyDeviceToHost));
+  if (J) PT_CUDA(cudaMemcpy(J, dJ, (size_t)2 * L * N * n * 8, cudaMemcpyDeviceToHost));
+  if (rmax) PT_CUDA(cudaMemcpy(rmax, dr, 8, cudaMemcpyDeviceToHost));
+  cudaFree(dx);
+  cudaFree(dh);
+  cudaFree(dJ);
+  cudaFree(dr);
+  return read_abort(p, W.ctl);
+}
+
+int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, const double* b, double* x) {
+  return guarded([&]() -> int {
+    if (!A || !b || !x || n < 1 || N < n || n > kMaxRowsPerThread * kThreads) return fail(PT_E_INVAL, "bad lstsq arguments");
+    int rc = check_device(device);
+    if (rc) return rc;
+    PT_CUDA(cudaSetDevice(device));
+    const int L = limbs(prec);
+    Layout lay = make_layout(L, n, N, 1);
+    double* dw = dev_alloc<double>(lay.dslice, &rc);
+    if (rc) return rc;
+    unsigned long long* uw = dev_alloc<unsigned long long>(lay.uslice, &rc);
+    int* dstat = dev_alloc<int>(1, &rc);
+    if (rc) return rc;
+    PT_CUDA(cudaMemset(dw, 0, lay.dslice * 8));
+    PT_CUDA(cudaMemset(uw, 0, lay.uslice * 8));
+    Work W = carve(dw, uw, lay, 0);
+    const long SA = (long)N * (n + 1), SJ = (long)N * n;
+    // [A | b] into SoA with stride SA
+    std::vector<double> hA((size_t)2 * L * SA);
+    for (int q = 0; q < 2 * L; ++q) {
+      std::memcpy(&hA[(size_t)q * SA], A + (size_t)q * SJ, SJ * 8);
+      std::memcpy(&hA[(size_t)q * SA + SJ], b + (size_t)q * N, (size_t)N * 8);
+    }
+    PT_CUDA(cudaMemcpy(W.A, hA.data(), hA.size() * 8, cudaMemcpyHostToDevice));
+    DevPlan dp{};
+    dp.n = n;
+    dp.N = N;
+    dp.P_mgs = ptplan::width_mgs(N);
+    const int gpc = kWarps / (dp.P_mgs / 32);
+    int per_sm = 0, sms = 0;
+    const void* fn = prec == PT_D ? (const void*)&k_lstsq<double> : prec == PT_DD ? (const void*)&k_lstsq<dd> : (const void*)&k_lstsq<qd>;
+    rc = occupancy_blocks(fn, device, &per_sm, &sms);
+    if (rc) return rc;
+    int blocks = std::min(std::min(sms, std::max(1, per_sm) * sms), std::max(1, (n + 1 + gpc - 1) / gpc));
+    unsigned long long epoch = 1;
+    void* args[] = {&dp, &W, &epoch, &dstat};
+    PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), args, 0, 0));
+    PT_CUDA(cudaDeviceSynchronize());
+    int st = 0;
+    PT_CUDA(cudaMemcpy(&st, dstat, 4, cudaMemcpyDeviceToHost));
+    if (st == 0) PT_CUDA(cudaMemcpy(x, W.dx, (size_t)2 * L * n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dw);
+    cudaFree(uw);
+    cudaFree(dstat);
+    if (st == PT_E_RANK) return fail(PT_E_RANK, "rank-deficient least-squares matrix");
+    if (st) return fail(st, "lstsq kernel failed");
+    return PT_OK;
+  });
+}
+
+int pt_arith_host(pt_prec prec, int32_t op, int64_t count, const double* a, const double* b, double* out) {
+  if (!a || !b || !out || count < 0) return PT_E_INVAL;
+  const int L = limbs(prec);
+  for (int64_t i = 0; i < count; ++i) {
+    const double* pa = a + i * 2 * L;
+    const double* pb = b + i * 2 * L;
+    double* po = out + i * 2 * L;
+    switch (prec) {
+      case PT_D: arith_one<double>(op, pa, pb, po); break;
+      case PT_DD: arith_one<dd>(op, pa, pb, po); break;
+      default: arith_one<qd>(op, pa, pb, po); break;
+    }
+  }
+  return PT_OK;
+}
+
+int pt_arith_device(int device, pt_prec prec, int32_t op, int64_t count, const double* a, const double* b,
+                    double* out) {
+  if (!a || !b || !out || count < 0) return fail(PT_E_INVAL, "bad arith args");
+  int rc = check_device(device);
+  if (rc) return rc;
+  PT_CUDA(cudaSetDevice(device));
+  const size_t bytes = (size_t)count * 2 * limbs(prec) * 8;
+  double *da = dev_alloc<double>(bytes / 8, &rc), *db = dev_alloc<double>(bytes / 8, &rc),
+         *dout = dev_alloc<double>(bytes / 8, &rc);
+  if (rc) return rc;
+  PT_CUDA(cudaMemcpy(da, a, bytes, cudaMemcpyHostToDevice));
+  PT_CUDA(cudaMemcpy(db, b, bytes, cudaMemcpyHostToDevice));
+  PT_CUDA(cudaMemset(dout, 0, bytes));
+  const int blocks = (int)std::min<int64_t>(4096, (count + 255) / 256 + 1);
+  switch (prec) {
+    case PT_D: k_arith<double><<<blocks, 256>>>(op, count, da, db, dout); break;
+    case PT_DD: k_arith<dd><<<blocks, 256>>>(op, count, da, db, dout); break;
+    default: k_arith<qd><<<blocks, 256>>>(op, count, da, db, dout); break;
+  }
+  PT_CUDA(cudaGetLastError());
+  PT_CUDA(cudaDeviceSynchronize());
+  PT_CUDA(cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost));
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(dout);
+  return PT_OK;
+}
+
+}  // extern "C"
