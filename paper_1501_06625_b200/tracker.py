@@ -123,9 +123,29 @@ class PolynomialSystem:
         nat.lib.pt_sysbuf_free(buf)
         return sysm
 
-    def _to_sysbuf(self):
-        """Round-trip through the generator buffer type (for pt_gen_augment)."""
-        raise NotImplementedError
+    @staticmethod
+    def from_terms(n_vars: int, equations, prec: PrecisionMode) -> "PolynomialSystem":
+        """Build from [[(support, coef), ...], ...] with support [(var, exp), ...]
+        (var ascending, exp >= 1) and coef a complex number or a (2, L) limb
+        array.  Term order is kept as given."""
+        L = prec.limbs
+        eq_ptr, term_ptr, var, exp, coefs = [0], [0], [], [], []
+        for eq in equations:
+            for sup, c in eq:
+                for v, e in sup:
+                    var.append(v)
+                    exp.append(e)
+                term_ptr.append(len(var))
+                cl = np.zeros((2, L))
+                if np.ndim(c) == 0:
+                    cl[0, 0], cl[1, 0] = complex(c).real, complex(c).imag
+                else:
+                    cl[:] = np.asarray(c, dtype=np.float64).reshape(2, L)
+                coefs.append(cl)
+            eq_ptr.append(len(term_ptr) - 1)
+        coef = np.stack(coefs, axis=-1) if coefs else np.zeros((2, L, 0))
+        return PolynomialSystem(n_vars, np.array(eq_ptr, np.int32), np.array(term_ptr, np.int32),
+                                np.array(var, np.int32), np.array(exp, np.int32), coef, prec)
 
 
 def _gen(fn, *args, prec: PrecisionMode) -> PolynomialSystem:

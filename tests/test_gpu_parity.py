@@ -1,0 +1,107 @@
+"""GPU parity: the CUDA path against the CPU oracle, bit for bit.
+
+Every comparison is exact (uint64 views of the binary64 limbs): the device
+replicates the reference operation sequences and the oracle's pinned
+summation trees, so any difference is a bug.
+"""
+import numpy as np
+import pytest
+
+from conftest import assert_bits_equal
+from arith_inputs import OPS, random_operands
+
+import paper_1501_06625_b200 as pt
+from paper_1501_06625_b200 import PrecisionMode as PM
+from paper_1501_06625_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+PRECS = [PM.D, PM.DD, PM.QD]
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=lambda p: p.name)
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "mul_d", "div", "sqrt", "renorm", "cmul", "cadd",
+                                "conj_mul", "norm_sqr", "modulus_double", "powi", "cscale", "cpowi"])
+def test_arith_device_bitwise(gpu, oracle, prec, op):
+    count = 4096 if prec == PM.QD else 20000
+    a = random_operands(int(prec), count, 1, positive=(op == "sqrt"), oracle=oracle)
+    b = random_operands(int(prec), count, 2, small_int=op in ("powi", "cpowi"), oracle=oracle)
+    want = oracle.arith(int(prec), OPS[op], a, b)
+    got = pt.arith(prec, OPS[op], a, b, device=gpu)
+    if op == "modulus_double":
+        want, got = want[:, 0, 0], got[:, 0, 0]
+    elif op in ("add", "sub", "mul", "mul_d", "div", "sqrt", "renorm", "norm_sqr", "powi"):
+        want, got = want[:, 0], got[:, 0]
+    assert_bits_equal(got, want, f"{prec.name} {op}")
+
+
+def _perturbed(w, scale=1e-3, seed=0):
+    rng = np.random.default_rng(seed)
+    x = np.array(w.start, copy=True)
+    x[:, 0, :] += scale * rng.uniform(-1, 1, size=x[:, 0, :].shape)
+    return x
+
+
+@pytest.mark.parametrize("name,prec,t", [("cyclic16", PM.DD, 0.37), ("cyclic16", PM.QD, 0.81),
+                                         ("chandra64", PM.D, 0.5), ("chandra64", PM.DD, 0.5),
+                                         ("chandra64", PM.QD, 0.25)])
+def test_eval_homotopy_bitwise(gpu, oracle, name, prec, t):
+    w = W.by_name(name, prec)
+    x = _perturbed(w)
+    h_ref, J_ref, r_ref = oracle.eval_homotopy(int(prec), w.g, w.f, w.gamma, w.k, x, t)
+    hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)
+    h, J, r = hom.evaluate(x, t)
+    assert_bits_equal(h, h_ref, "h")
+    assert_bits_equal(J, J_ref, "J")
+    assert_bits_equal(np.array([r]), np.array([r_ref]), "max|h|")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=lambda p: p.name)
+@pytest.mark.parametrize("N,n", [(4, 4), (19, 16), (64, 64), (97, 96), (40, 33)])
+def test_lstsq_bitwise(gpu, oracle, prec, N, n):
+    rng = np.random.default_rng(N * 1000 + n)
+    L = prec.limbs
+    A = np.zeros((2, L, N * n))
+    b = np.zeros((2, L, N))
+    A[:, 0] = rng.uniform(-1, 1, (2, N * n))
+    b[:, 0] = rng.uniform(-1, 1, (2, N))
+    want = oracle.lstsq(int(prec), A, b)
+    got = pt.least_squares_solve(A, b, prec, device=gpu)
+    assert_bits_equal(got, want, "x")
+
+
+def _compare_track(w, out, end_ref, st_ref, tr_ref):
+    assert out.success == (st_ref.status == 0)
+    assert (out.steps, out.accepted, out.newton_iters, out.start_iters) == (
+        st_ref.steps, st_ref.accepted, st_ref.newton_iters, st_ref.start_iters)
+    assert_bits_equal(np.array([out.final_residual, out.final_update, out.t_end]),
+                      np.array([st_ref.final_residual, st_ref.final_update, st_ref.t_end]), "stats")
+    assert len(out.trace) == len(tr_ref)
+    for a, b in zip(out.trace, tr_ref):
+        assert (a.ok, a.iters) == (b.ok, b.iters)
+        assert_bits_equal(np.array([a.t, a.residual, a.update]), np.array([b.t, b.residual, b.update]), "trace")
+    assert_bits_equal(out.end, end_ref, "end point")
+
+
+@pytest.mark.parametrize("name,prec", [("cyclic16", PM.DD), ("cyclic16", PM.D), ("chandra64", PM.D),
+                                       ("chandra64", PM.DD), ("chandra64", PM.QD)])
+def test_track_path_bitwise(gpu, oracle, name, prec):
+    w = W.by_name(name, prec)
+    cap = w.params.max_steps + 2
+    end_ref, st_ref, tr_ref = oracle.track_path(int(prec), w.g, w.f, w.gamma, w.k, w.start, w.params, cap)
+    hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)
+    out = hom.track_path(w.start, w.params, trace=True)
+    _compare_track(w, out, end_ref, st_ref, tr_ref)
+    if name == "chandra64":
+        assert out.success
+
+
+def test_track_batch_bitwise(gpu, oracle):
+    w = W.random_system(n=8, degree=3, n_monomials=40, prec=PM.DD, n_paths=48)
+    hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)
+    ends, outs = hom.track_batch(w.starts, w.params)
+    for p in range(w.starts.shape[0]):
+        end_ref, st_ref, _ = oracle.track_path(int(w.prec), w.g, w.f, w.gamma, w.k, w.starts[p], w.params)
+        assert (outs[p].steps, outs[p].newton_iters, outs[p].success) == (st_ref.steps, st_ref.newton_iters,
+                                                                         st_ref.status == 0)
+        assert_bits_equal(ends[p], end_ref, f"path {p}")
