@@ -97,6 +97,8 @@ typedef struct {
   int32_t accepted;        /* accepted trials */
   int32_t newton_iters;    /* evaluations, start validation included */
   int32_t start_iters;     /* evaluations of the t=0 start validation */
+  int32_t solves;          /* completed least-squares solves (MGS + back substitution) */
+  int32_t reserved;
   double final_residual;   /* last max|h| computed */
   double final_update;     /* last max|dx| computed (-1 if none) */
   double t_end;            /* last accepted t */
@@ -127,6 +129,18 @@ void pt_plan_destroy(pt_plan* plan);
 /* Query plan facts: 0 n_vars, 1 n_eqs, 2 monomials, 3 contributions,
  * 4 grid CTAs used for one path, 5 precision, 6 batch CTAs resident. */
 int64_t pt_plan_info(const pt_plan* plan, int32_t what);
+
+/* Algorithmic work of one unit of the path, counted on the reference
+ * algorithms.  kind: 0 one evaluation (h and J),
+ * 1 one least-squares solve + update, 2 one prediction of degree `degree`.
+ * out[0..4]: real adds, real muls, real divisions, real square roots,
+ * binary64 hypots; out[5]: FP64 arithmetic instructions of the reference
+ * DD/QD algorithms for those operations in the plan's precision. */
+int pt_plan_work(const pt_plan* plan, int32_t kind, int32_t degree, double* out);
+
+/* Measured FP64-pipe peak of `device`: thread-level DFMA instructions per
+ * second from an unrolled independent-chain microbenchmark. */
+int pt_fp64_peak(int device, double* instr_per_s, double* ms);
 
 /* Enable a per-trial trace of up to `capacity` events (0 disables). */
 int pt_plan_set_trace(pt_plan* plan, int32_t capacity);

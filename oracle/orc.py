@@ -35,7 +35,7 @@ class StepParams(C.Structure):
 
 class PathStats(C.Structure):
     _fields_ = [("status", C.c_int32), ("failure_kind", C.c_int32), ("steps", C.c_int32),
-                ("accepted", C.c_int32), ("newton_iters", C.c_int32), ("start_iters", C.c_int32),
+                ("accepted", C.c_int32), ("newton_iters", C.c_int32), ("start_iters", C.c_int32), ("solves", C.c_int32), ("reserved", C.c_int32),
                 ("final_residual", C.c_double), ("final_update", C.c_double), ("t_end", C.c_double)]
 
 

@@ -59,7 +59,7 @@ struct StepParams {  // same layout as pt_step_params
 };
 
 struct PathStats {  // same layout as pt_path_stats
-  int32_t status, failure_kind, steps, accepted, newton_iters, start_iters;
+  int32_t status, failure_kind, steps, accepted, newton_iters, start_iters, solves, reserved;
   double final_residual, final_update, t_end;
 };
 
@@ -396,11 +396,12 @@ struct Tracker {
     bool ok;
     int kind, iters;
     double residual, update;
+    int solves;
   };
 
   // newton_correct, Fig. 2.
   NewtonOutcome newton(std::vector<C>& x, double t, const StepParams& P) const {
-    NewtonOutcome o{false, NW_ITERATION_BUDGET, 0, -1.0, -1.0};
+    NewtonOutcome o{false, NW_ITERATION_BUDGET, 0, -1.0, -1.0, 0};
     double last = std::numeric_limits<double>::infinity();
     std::vector<C> Amat, dx;
     for (int it = 1; it <= P.newton_max_iter; ++it) {
@@ -420,6 +421,7 @@ struct Tracker {
         o.kind = NW_LINEAR_SOLVE;
         return o;
       }
+      ++o.solves;
       double u = 0.0;
       for (int i = 0; i < n; ++i) u = nan_max(u, A::modulus_double(dx[i]));
       o.update = u;
@@ -468,6 +470,7 @@ struct Tracker {
     NewtonOutcome o = newton(x, 0.0, P);  // start validation
     st.start_iters = o.iters;
     st.newton_iters = o.iters;
+    st.solves = o.solves;
     st.final_residual = o.residual;
     st.final_update = o.update;
     if (!o.ok) {
@@ -494,6 +497,7 @@ struct Tracker {
       predict(ht, hx, ttrial, xp);
       o = newton(xp, ttrial, P);
       st.newton_iters += o.iters;
+      st.solves += o.solves;
       st.final_residual = o.residual;
       st.final_update = o.update;
       if (trace) trace->push_back({ttrial, o.ok ? 1 : 0, o.iters, o.residual, o.update});

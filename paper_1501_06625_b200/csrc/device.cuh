@@ -631,21 +631,22 @@ __device__ __forceinline__ double kSqrtEps<qd>() {
 struct NewtonOut {
   int ok, kind, iters;
   double residual, update;
+  int solves;
 };
 
 template <class R, class Team>
 __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh,
                             const pt_step_params& sp, double t, unsigned long long& epoch) {
-  NewtonOut o{0, NW_ITERATION_BUDGET, 0, -1.0, -1.0};
+  NewtonOut o{0, NW_ITERATION_BUDGET, 0, -1.0, -1.0, 0};
   const double sqrt_eps = kSqrtEps<R>();
   double last = bitsd(0x7ff0000000000000ull);
   const int tid = team.block * kThreads + threadIdx.x, nth = team.nblocks * kThreads;
   for (int it = 1; it <= sp.newton_max_iter; ++it) {
     o.iters = it;
     eval_monomials<R>(P, W, tid, nth);
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     eval_slots<R, Team>(P, W, team, sh, t);
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     double r = 0.0;
     for (int i = threadIdx.x; i < P.N; i += kThreads) r = nan_max(r, W.hmod[i]);
     r = block_nan_max(r, sh.red);
@@ -661,7 +662,7 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
     }
     ++epoch;
     mgs<R, Team>(P, W, team, sh, epoch, sqrt_eps);
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     if (ld_acquire(W.ctl + CTL_RANK) == epoch) {
       o.kind = NW_LINEAR_SOLVE;
       return o;
@@ -670,8 +671,9 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       const double u = backsub_update<R>(P, W, sh);
       if (threadIdx.x == 0) W.scal[0] = u;
     }
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     const double u = *(volatile double*)(W.scal);
+    ++o.solves;
     o.update = u;
     if (u < sp.newton_tol) {
       o.ok = 1;
@@ -706,6 +708,7 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
   if (o.kind == NW_ABORT) return;
   st.start_iters = o.iters;
   st.newton_iters = o.iters;
+  st.solves = o.solves;
   st.final_residual = o.residual;
   st.final_update = o.update;
   History H;
@@ -737,6 +740,7 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
       o = newton<R, Team>(P, W, team, sh, sp, ttrial, epoch);
       if (o.kind == NW_ABORT) return;
       st.newton_iters += o.iters;
+      st.solves += o.solves;
       st.final_residual = o.residual;
       st.final_update = o.update;
       if (leader && threadIdx.x == 0 && io.trace && ntrace < io.trace_cap)

@@ -39,6 +39,15 @@
 
 namespace ptk {
 
+#if defined(PT_COUNT_FP64) && !defined(__CUDA_ARCH__)
+// host-only instrumentation (tools/count_fp64.cpp): FP64 arithmetic
+// instructions executed, i.e. the roofline work unit of DESIGN.md section 4
+inline unsigned long long g_fp64 = 0;
+#define PT_TICK() (++::ptk::g_fp64)
+#else
+#define PT_TICK() ((void)0)
+#endif
+
 // ---------------------------------------------------------------------------
 // binary64 primitives with pinned rounding
 // ---------------------------------------------------------------------------
@@ -46,6 +55,7 @@ PT_HD double add64(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __dadd_rn(a, b);
 #else
+  PT_TICK();
   return a + b;
 #endif
 }
@@ -53,6 +63,7 @@ PT_HD double sub64(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __dsub_rn(a, b);
 #else
+  PT_TICK();
   return a - b;
 #endif
 }
@@ -60,6 +71,7 @@ PT_HD double mul64(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __dmul_rn(a, b);
 #else
+  PT_TICK();
   return a * b;
 #endif
 }
@@ -67,6 +79,7 @@ PT_HD double fma64(double a, double b, double c) {
 #if defined(__CUDA_ARCH__)
   return __fma_rn(a, b, c);
 #else
+  PT_TICK();
   return std::fma(a, b, c);
 #endif
 }
@@ -74,6 +87,7 @@ PT_HD double div64(double a, double b) {
 #if defined(__CUDA_ARCH__)
   return __ddiv_rn(a, b);
 #else
+  PT_TICK();
   return a / b;
 #endif
 }
@@ -81,6 +95,7 @@ PT_HD double sqrt64(double a) {
 #if defined(__CUDA_ARCH__)
   return __dsqrt_rn(a);
 #else
+  PT_TICK();
   return std::sqrt(a);
 #endif
 }

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "device.cuh"
+#include "work.hpp"
 
 using namespace ptdev;
 
@@ -229,6 +230,23 @@ __global__ void k_arith(int op, long count, const double* a, const double* b, do
     arith_one<R>(op, a + i * 2 * L, b + i * 2 * L, out + i * 2 * L);
 }
 
+// FP64-pipe peak: kPeakChains independent DFMA chains per thread.
+constexpr int kPeakChains = 8;
+__global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters) {
+  double a[kPeakChains];
+#pragma unroll
+  for (int c = 0; c < kPeakChains; ++c) a[c] = 1e-3 * (threadIdx.x + c);
+  const double b = 0.9999999, d = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kPeakChains; ++c) a[c] = __fma_rn(a[c], b, d);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < kPeakChains; ++c) s += a[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // ---------------------------------------------------------------------------
 // plan object
 // ---------------------------------------------------------------------------
@@ -262,6 +280,7 @@ struct pt_plan {
   pt_path_stats* b_stats = nullptr;
   long b_cap = 0;
   unsigned long long launches = 0;
+  ptwork::OpCount w_eval, w_solve;
 };
 
 namespace {
@@ -406,6 +425,8 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     p->N = hp.N;
     p->M = (int)hp.mono_size.size();
     p->n_ctr = (long)hp.ctr_coef.size();
+    p->w_eval = ptwork::eval_work(hp, relax_k);
+    p->w_solve = ptwork::solve_work(hp.N, hp.n);
     PT_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     // tables: one allocation, 256-byte aligned pieces
     std::vector<std::pair<const void*, size_t>> pieces = {
@@ -500,6 +521,50 @@ int64_t pt_plan_info(const pt_plan* p, int32_t what) {
     case 7: return p->dp.ws_len;
   }
   return -1;
+}
+
+int pt_plan_work(const pt_plan* p, int32_t kind, int32_t degree, double* out) {
+  if (!p || !out || kind < 0 || kind > 2 || degree < 0) return PT_E_INVAL;
+  const ptwork::OpCount o = kind == 0 ? p->w_eval : kind == 1 ? p->w_solve : ptwork::predict_work(p->n, degree);
+  out[0] = o.radd;
+  out[1] = o.rmul;
+  out[2] = o.rdiv;
+  out[3] = o.rsqrt;
+  out[4] = o.hypot;
+  out[5] = ptwork::fp64_instructions(o, p->L);
+  return PT_OK;
+}
+
+int pt_fp64_peak(int device, double* instr_per_s, double* ms_out) {
+  if (!instr_per_s) return PT_E_INVAL;
+  int rc = check_device(device);
+  if (rc) return rc;
+  PT_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  PT_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int blocks = prop.multiProcessorCount * 4, threads = 256, iters = 4096;
+  double* d = dev_alloc<double>((size_t)blocks * threads, &rc);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  PT_CUDA(cudaEventCreate(&e0));
+  PT_CUDA(cudaEventCreate(&e1));
+  k_fp64_peak<<<blocks, threads>>>(d, iters);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    PT_CUDA(cudaEventRecord(e0));
+    k_fp64_peak<<<blocks, threads>>>(d, iters);
+    PT_CUDA(cudaEventRecord(e1));
+    PT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  *instr_per_s = (double)blocks * threads * iters * kPeakChains / (best * 1e-3);
+  if (ms_out) *ms_out = best;
+  return PT_OK;
 }
 
 int pt_plan_set_trace(pt_plan* p, int32_t capacity) {
