@@ -58,15 +58,15 @@ def workload(args):
     from paper_1501_06625_b200 import PrecisionMode, workloads as W
     prec = PrecisionMode.parse(args.prec) if args.prec else None
     if args.workload == "cyclic16":
-        return W.cyclic_leg(4, prec or PrecisionMode.DD)
+        return W.cyclic_leg(4, (prec if prec is not None else PrecisionMode.DD))
     if args.workload == "cyclic256":
-        return W.cyclic_leg(16, prec or PrecisionMode.QD)
+        return W.cyclic_leg(16, (prec if prec is not None else PrecisionMode.QD))
     if args.workload == "chandra64":
-        return W.chandra(64, prec or PrecisionMode.DD)
+        return W.chandra(64, (prec if prec is not None else PrecisionMode.DD))
     if args.workload == "rand96":
-        return W.random_system(96, 4, 65536, prec or PrecisionMode.DD)
+        return W.random_system(96, 4, 65536, (prec if prec is not None else PrecisionMode.DD))
     if args.workload == "batch32":
-        return W.batch(prec=prec or PrecisionMode.DD)
+        return W.batch(prec=(prec if prec is not None else PrecisionMode.DD))
     raise SystemExit(f"unknown workload {args.workload}")
 
 
@@ -234,7 +234,7 @@ def run_ours(args):
     batch = args.workload == "batch32"
     hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=device)
     sp = w.params.native()
-    stream = torch.cuda.current_stream(device)
+    stream = torch.cuda.Stream(device)  # kernel and its CUDA events on the same stream
     sh = C.c_void_p(stream.cuda_stream)
     if batch:
         P = w.starts.shape[0]
@@ -262,18 +262,23 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize(device)
 
-    for _ in range(args.warmup):
-        launch()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            launch()
     barrier()
     clocks = Clocks(device)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
+    prof = np.zeros(8)
+    nat.check(nat.lib.pt_plan_profile(hom.plan, nat.dptr(prof), 1))
     for e0, e1 in ev:
-        flush.zero_()
-        e0.record(stream)
-        launch()
-        e1.record(stream)
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0.record(stream)
+            launch()
+            e1.record(stream)
     barrier()
+    nat.check(nat.lib.pt_plan_profile(hom.plan, nat.dptr(prof), 1))
     clk = clocks.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     t_dev = sum(step_ms) / 1e3
@@ -341,6 +346,10 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "work_per_launch_fp64_instr": work, "work_per_eval": we, "work_per_solve": ws},
             "gpu_launches": args.steps,
+            "phase_ms_per_path": None if batch else {
+                k: prof[i] * 1e-6 / args.steps for i, k in enumerate(
+                    ["monomials", "slot_sums", "mgs", "backsub_update", "predict"])},
+            "newton_iters_timed": None if batch else prof[5] / args.steps,
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:

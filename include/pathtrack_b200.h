@@ -127,8 +127,16 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
 void pt_plan_destroy(pt_plan* plan);
 
 /* Query plan facts: 0 n_vars, 1 n_eqs, 2 monomials, 3 contributions,
- * 4 grid CTAs used for one path, 5 precision, 6 batch CTAs resident. */
+ * 4 grid CTAs used for one path, 5 precision, 6 batch CTAs resident,
+ * 7 monomial workspace entries, 8 single-path engine (0 grid, 1 cluster),
+ * 9 cluster size of the cluster engine (0: none schedulable). */
 int64_t pt_plan_info(const pt_plan* plan, int32_t what);
+
+/* Force the single-path engine: 0 = cooperative persistent grid (all SMs,
+ * grid barriers, L2 flags), 1 = one thread-block cluster (cluster barriers,
+ * DSMEM column exchange).  pt_plan_create picks one by problem size; both
+ * produce bit-identical results. */
+int pt_plan_set_engine(pt_plan* plan, int32_t engine);
 
 /* Algorithmic work of one unit of the path, counted on the reference
  * algorithms.  kind: 0 one evaluation (h and J),
@@ -141,6 +149,19 @@ int pt_plan_work(const pt_plan* plan, int32_t kind, int32_t degree, double* out)
 /* Measured FP64-pipe peak of `device`: thread-level DFMA instructions per
  * second from an unrolled independent-chain microbenchmark. */
 int pt_fp64_peak(int device, double* instr_per_s, double* ms);
+
+/* Latency microbenchmarks used to size the design:
+ * what 0: cycles per dependent op, out[0] DADD, [1] DD add, [2] DD mul,
+ * [3] QD add, [4] QD mul, [5] complex DD mul, [6] hypot;
+ * what 1: out[0] ns per grid barrier (148 CTAs); what 2: out[0] one-way ns of
+ * a release/acquire flag between CTA 0 and the last CTA. */
+int pt_microbench(int device, int32_t what, double* out);
+
+/* Device phase timers of the single-path kernel (block 0, globaltimer ns,
+ * accumulated over launches): out[0] monomials, [1] slot sums + residual,
+ * [2] MGS, [3] back substitution + update, [4] predictor, [5] Newton
+ * iterations (count); reset != 0 clears them. */
+int pt_plan_profile(pt_plan* plan, double* out, int32_t reset);
 
 /* Enable a per-trial trace of up to `capacity` events (0 disables). */
 int pt_plan_set_trace(pt_plan* plan, int32_t capacity);

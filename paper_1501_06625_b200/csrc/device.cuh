@@ -17,6 +17,7 @@
 //   - Newton Fig. 2, tracker Fig. 3 with SPEC.md:492-495.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,9 +32,10 @@ using namespace ptk;
 
 constexpr int kThreads = 256;  // every tracker CTA
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxRowsPerThread = 4;  // n <= 1024
+constexpr int kMaxRowsPerThread = 2;  // n <= 512
 constexpr int kMaxDegree = 8;
 constexpr double kTimeoutNs = 20e9;
+constexpr int kMaxCols = 520;  // n + 1 <= 513 MGS columns (shared flag arrays)
 
 enum { CTL_BAR_COUNT = 0, CTL_BAR_GEN = 1, CTL_ABORT = 2, CTL_RANK = 3, CTL_QUEUE = 4, CTL_WORDS = 8 };
 enum { NW_OK = 0, NW_RESIDUAL_INCREASE = 1, NW_ITERATION_BUDGET = 2, NW_LINEAR_SOLVE = 3, NW_ABORT = 4 };
@@ -56,6 +58,7 @@ struct DevPlan {
   long n_coef;
   const double* gamma;  // 2L limbs
   int relax_k;
+  int mgs_smem;  // 1: MGS keeps owned columns in dynamic shared memory
 };
 
 // One path's workspace.  All arrays are complex SoA unless noted.
@@ -72,6 +75,28 @@ struct Work {
   double* dx;     // [2L][n] last Newton update
   unsigned long long* flags;  // [n+1] MGS column-ready flags (epoch values)
   unsigned long long* ctl;    // [CTL_WORDS] barrier / abort / rank-fail
+  unsigned long long* prof;   // [kProfSlots] phase time accumulators (ns, block 0)
+};
+
+// Phase timers: block 0 / thread 0 accumulates globaltimer deltas.
+enum { PROF_MONO = 0, PROF_SLOTS = 1, PROF_MGS = 2, PROF_BACKSUB = 3, PROF_PREDICT = 4, PROF_ITERS = 5, kProfSlots = 8 };
+struct PhaseClock {
+  unsigned long long t;
+  bool on;
+  __device__ PhaseClock(bool enable) : t(0), on(enable) {
+    if (on) t = gtimer_raw();
+  }
+  __device__ static unsigned long long gtimer_raw() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+  }
+  __device__ void lap(unsigned long long* acc) {
+    if (!on) return;
+    const unsigned long long now = gtimer_raw();
+    *acc += now - t;
+    t = now;
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -94,43 +119,142 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long atom_add_release(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
+// Wait until the flag word carries (epoch << 1) | bit; returns the bit
+// (1 = the column failed the rank test), or -1 on abort / watchdog.
+__device__ __forceinline__ int wait_flag(const unsigned long long* flag, unsigned long long epoch,
+                                         unsigned long long* ctl) {
+  const unsigned long long t0 = gtimer();
+  unsigned int spins = 0;
+  for (;;) {
+    const unsigned long long v = ld_acquire(flag);
+    if ((v >> 1) == epoch) return (int)(v & 1ull);
+    if ((++spins & 255u) == 0) {
+      if (ld_acquire(ctl + CTL_ABORT)) return -1;
+      if ((double)(gtimer() - t0) > kTimeoutNs) {
+        atomicExch(ctl + CTL_ABORT, 1ull);
+        return -1;
+      }
+    }
+  }
+}
+
+// --- shared-memory (DSMEM) primitives for the cluster engine ---------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_release_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t cta_addr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(cta_addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nranks() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+// A team runs one path.  Besides a barrier it provides the MGS column
+// exchange: publish(k) after the owner group has normalised column k,
+// wait(k) before a consumer reads q_k, and q_src(k) = where q_k can be read.
+//
+// GridTeam: cooperative persistent grid; q_k is copied to the global matrix
+// and announced by a release flag in global memory (through L2).
 struct GridTeam {
   unsigned long long* ctl;
   int nblocks, block;
   static constexpr bool kGrid = true;
-  // Sense-free generation barrier; returns false once any CTA has aborted.
+  static constexpr bool kQInGlobal = true;
+  uint32_t* sflags;  // unused
+  // Generation barrier; returns false once any CTA has aborted.
   __device__ bool sync(int* s_flag) const {
     __syncthreads();
     if (threadIdx.x == 0) {
       int abort = 0;
       const unsigned long long gen = ld_acquire(ctl + CTL_BAR_GEN);
-      __threadfence();
-      const unsigned long long arrived = atomicAdd(ctl + CTL_BAR_COUNT, 1ull);
+      const unsigned long long arrived = atom_add_release(ctl + CTL_BAR_COUNT, 1ull);
       if (arrived == (unsigned long long)(nblocks - 1)) {
         atomicExch(ctl + CTL_BAR_COUNT, 0ull);
-        __threadfence();
         st_release(ctl + CTL_BAR_GEN, gen + 1);
       } else {
         const unsigned long long t0 = gtimer();
+        unsigned int spins = 0;
         while (ld_acquire(ctl + CTL_BAR_GEN) == gen) {
-          if (ld_acquire(ctl + CTL_ABORT)) {
-            abort = 1;
-            break;
+          if ((++spins & 255u) == 0) {
+            if (ld_acquire(ctl + CTL_ABORT)) {
+              abort = 1;
+              break;
+            }
+            if ((double)(gtimer() - t0) > kTimeoutNs) {
+              atomicExch(ctl + CTL_ABORT, 1ull);
+              abort = 1;
+              break;
+            }
           }
-          if ((double)(gtimer() - t0) > kTimeoutNs) {
-            atomicExch(ctl + CTL_ABORT, 1ull);
-            abort = 1;
-            break;
-          }
-          __nanosleep(32);
         }
       }
       __threadfence();
-      if (ld_acquire(ctl + CTL_ABORT)) abort = 1;
       *s_flag = abort;
     }
     __syncthreads();
     return *s_flag == 0;
+  }
+  __device__ void publish(unsigned long long* flags, int k, unsigned long long epoch, int fail) const {
+    st_release(flags + k, (epoch << 1) | (unsigned long long)fail);
+  }
+  __device__ int wait(const unsigned long long* flags, int k, unsigned long long epoch) const {
+    return wait_flag(flags + k, epoch, ctl);
+  }
+};
+
+// ClusterTeam: one thread-block cluster (<= 16 CTAs) runs the path.  Barrier
+// = barrier.cluster; q_k stays in the owner CTA's shared memory and is read
+// through DSMEM; the owner pushes a release flag into every CTA's shared
+// flag array, so consumers poll locally.
+struct ClusterTeam {
+  unsigned long long* ctl;
+  int nblocks, block;
+  static constexpr bool kGrid = false;
+  static constexpr bool kQInGlobal = false;
+  uint32_t* sflags;  // [n+1] per CTA (shared memory)
+  __device__ bool sync(int*) const {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    return true;
+  }
+  __device__ void publish(unsigned long long*, int k, unsigned long long epoch, int fail) const {
+    const uint32_t v = ((uint32_t)(epoch & 0x7fffffffull) << 1) | (uint32_t)fail;
+    const uint32_t local = smem_u32(sflags + k);
+    for (int r = 0; r < nblocks; ++r) st_release_cluster_u32(mapa_u32(local, (uint32_t)r), v);
+  }
+  __device__ int wait(const unsigned long long*, int k, unsigned long long epoch) const {
+    const uint32_t want = (uint32_t)(epoch & 0x7fffffffull);
+    const uint32_t a = smem_u32(sflags + k);
+    const unsigned long long t0 = gtimer();
+    unsigned int spins = 0;
+    for (;;) {
+      const uint32_t v = ld_acquire_cluster_u32(a);
+      if ((v >> 1) == want) return (int)(v & 1u);
+      if ((++spins & 1023u) == 0 && (double)(gtimer() - t0) > kTimeoutNs) {
+        atomicExch(ctl + CTL_ABORT, 1ull);
+        __trap();  // hardware cluster barriers cannot be abandoned: kill the launch instead of hanging
+      }
+    }
   }
 };
 
@@ -138,27 +262,27 @@ struct BlockTeam {
   unsigned long long* ctl;
   int nblocks, block;  // 1, 0
   static constexpr bool kGrid = false;
+  static constexpr bool kQInGlobal = false;
+  uint32_t* sflags;  // [n+1] shared memory
   __device__ bool sync(int*) const {
     __syncthreads();
     return true;
   }
-};
-
-// Wait for column flag == epoch (one thread spins, the group then syncs).
-__device__ __forceinline__ bool wait_flag(const unsigned long long* flag, unsigned long long epoch,
-                                          unsigned long long* ctl) {
-  const unsigned long long t0 = gtimer();
-  while (ld_acquire(flag) != epoch) {
-    if (ld_acquire(ctl + CTL_ABORT)) return false;
-    if ((double)(gtimer() - t0) > kTimeoutNs) {
-      atomicExch(ctl + CTL_ABORT, 1ull);
-      return false;
-    }
-    __nanosleep(20);
+  __device__ void publish(unsigned long long*, int k, unsigned long long epoch, int fail) const {
+    __threadfence_block();
+    *(volatile uint32_t*)(sflags + k) = ((uint32_t)(epoch & 0x7fffffffull) << 1) | (uint32_t)fail;
   }
-  __threadfence();
-  return true;
-}
+  __device__ int wait(const unsigned long long*, int k, unsigned long long epoch) const {
+    const uint32_t want = (uint32_t)(epoch & 0x7fffffffull);
+    for (;;) {
+      const uint32_t v = *(volatile uint32_t*)(sflags + k);
+      if ((v >> 1) == want) {
+        __threadfence_block();
+        return (int)(v & 1u);
+      }
+    }
+  }
+};
 
 // ---------------------------------------------------------------------------
 // shuffles and group reductions of reals / complex values
@@ -412,19 +536,43 @@ __device__ cplx<R> group_bcast_c(const Group& g, int gi, const cplx<R>& v, Smem<
   return r;
 }
 
-// Normalise column k (already projected against q_0..q_{k-1}) and publish it.
-// Returns false on rank deficiency (flag still published so nobody hangs).
+// Column storage during MGS: owned columns live in shared memory (SoA, stride
+// N) when they fit, else in place in the global matrix (stride N*(n+1)).
+struct ColRef {
+  double* p;
+  long S;
+};
+
+template <class R>
+__device__ __forceinline__ cplx<R> ldcg_c(const double* p, long S, long i) {
+  constexpr int L = limbs_of<R>::L;
+  cplx<R> v;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    r_set_limb(v.re, l, __ldcg(p + l * S + i));
+    r_set_limb(v.im, l, __ldcg(p + (L + l) * S + i));
+  }
+  return v;
+}
+
+constexpr int kMaxElems = 4;  // ceil(N / P_mgs) <= 4  (N <= 1024)
+
+// Normalise column k (already projected against q_0..q_{k-1}), write q_k to
+// the global matrix and publish it.  Returns false on rank deficiency (the
+// flag is still published so nobody hangs).
 template <class R, class Team>
-__device__ bool mgs_normalize(const DevPlan& P, const Work& W, const Team& team, const Group& g, int gi,
-                              Smem<R>& sh, int& phase, int k, unsigned long long epoch, double sqrt_eps) {
+__device__ bool mgs_normalize(const DevPlan& P, const Work& W, const Team& team, const Group& g, int gi, Smem<R>& sh,
+                              int& phase, const ColRef& c, bool q_to_global, int k, unsigned long long epoch,
+                              double sqrt_eps) {
   const int N = P.N, Pm = P.P_mgs;
   const long SA = (long)N * (P.n + 1);
-  const double* colk = W.A + (long)k * N;
   R acc = rconst<R>(0.0);
-  if (g.p < Pm && g.p < N) {
-    for (int i = g.p; i < N; i += Pm) {
-      const R v = c_norm_sqr(load_c<R>(colk, SA, i));
-      acc = (i == g.p) ? v : r_add(acc, v);
+#pragma unroll
+  for (int r = 0; r < kMaxElems; ++r) {
+    const int i = g.p + r * Pm;
+    if (i < N) {
+      const R v = c_norm_sqr(load_c<R>(c.p, c.S, i));
+      acc = (r == 0) ? v : r_add(acc, v);
     }
   }
   R* rsm = reinterpret_cast<R*>(sh.tree + (gi * 32 * g.gw));
@@ -434,7 +582,7 @@ __device__ bool mgs_normalize(const DevPlan& P, const Work& W, const Team& team,
   if (g.p == 0) {
     const R rkk = r_sqrt(nrm2);
     const double d = r_hi(rkk);
-    const double prev = k > 0 ? W.rmaxp[k - 1] : 0.0;
+    const double prev = k > 0 ? __ldcg(W.rmaxp + k - 1) : 0.0;
     const double mx = d > prev ? d : prev;
     ok = d > sqrt_eps * mx;
     W.rmaxp[k] = mx;
@@ -448,30 +596,38 @@ __device__ bool mgs_normalize(const DevPlan& P, const Work& W, const Team& team,
   inv = group_bcast_r<R>(g, gi, inv, sh, phase);
   ok = sh.ibcast[gi][phase ^ 1];
   if (ok) {
-    double* ck = W.A + (long)k * N;
-    for (int i = g.p; i < N; i += 32 * g.gw) store_c<R>(ck, SA, i, c_scale(load_c<R>(ck, SA, i), inv));
+    double* gk = W.A + (long)k * N;
+#pragma unroll
+    for (int r = 0; r < kMaxElems; ++r) {
+      const int i = g.p + r * Pm;
+      if (i < N) {
+        const cplx<R> q = c_scale(load_c<R>(c.p, c.S, i), inv);
+        store_c<R>(c.p, c.S, i, q);
+        if (q_to_global && c.p != gk) store_c<R>(gk, SA, i, q);
+      }
+    }
   }
   g.sync();
   if (g.p == 0) {
     if (!ok) atomicExch(W.ctl + CTL_RANK, epoch);
-    __threadfence();
-    st_release(W.flags + k, epoch);
+    team.publish(W.flags, k, epoch, !ok);  // release: cumulative over the group's writes (bar.sync above)
   }
   return ok != 0;
 }
 
-template <class R, class Team>
+// r_kj = q_k^H a_j (canonical width P_mgs), a_j -= r_kj q_k.  q: this thread's
+// elements of q_k (rows p + r*P_mgs).
+template <class R>
 __device__ void mgs_project(const DevPlan& P, const Work& W, const Group& g, int gi, Smem<R>& sh, int& phase,
-                            int k, int j) {
+                            const cplx<R>* q, const ColRef& c, int k, int j) {
   const int N = P.N, n = P.n, Pm = P.P_mgs;
-  const long SA = (long)N * (n + 1);
-  const double* qk = W.A + (long)k * N;
-  double* aj = W.A + (long)j * N;
   cplx<R> acc = c_zero<R>();
-  if (g.p < Pm && g.p < N) {
-    for (int i = g.p; i < N; i += Pm) {
-      const cplx<R> v = c_conj_mul(load_c<R>(qk, SA, i), load_c<R>(aj, SA, i));
-      acc = (i == g.p) ? v : c_add(acc, v);
+#pragma unroll
+  for (int r = 0; r < kMaxElems; ++r) {
+    const int i = g.p + r * Pm;
+    if (i < N) {
+      const cplx<R> v = c_conj_mul(q[r], load_c<R>(c.p, c.S, i));
+      acc = (r == 0) ? v : c_add(acc, v);
     }
   }
   cplx<R>* sm = sh.tree + gi * 32 * g.gw;
@@ -479,82 +635,137 @@ __device__ void mgs_project(const DevPlan& P, const Work& W, const Group& g, int
   if (g.p == 0) store_c<R>(W.Rm, (long)n * (n + 1), (long)j * n + k, rkj);
   rkj = group_bcast_c<R>(g, gi, rkj, sh, phase);
   if (j < n || k < n - 1) {
-    for (int i = g.p; i < N; i += 32 * g.gw)
-      store_c<R>(aj, SA, i, c_sub(load_c<R>(aj, SA, i), c_mul(rkj, load_c<R>(qk, SA, i))));
+#pragma unroll
+    for (int r = 0; r < kMaxElems; ++r) {
+      const int i = g.p + r * Pm;
+      if (i < N) store_c<R>(c.p, c.S, i, c_sub(load_c<R>(c.p, c.S, i), c_mul(rkj, q[r])));
+    }
   }
-  g.sync();
 }
 
 // Column-pipelined right-looking MGS.  Column j is owned
-// by group j mod G; the owner of column k+1 normalises it as soon as q_k has
-// been applied, so the sqrt/reciprocal chain overlaps the bulk updates.
+// by group j mod G (group id = block + nblocks * group-in-CTA, so
+// consecutive columns sit on different SMs); the owner keeps its columns in
+// shared memory for the whole factorisation, normalises column k+1 as soon
+// as q_k has been applied (look-ahead), and publishes q_{k+1} with a release
+// flag.  Consumers read each q_k once from L2 into registers.
 template <class R, class Team>
-__device__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, unsigned long long epoch,
-                    double sqrt_eps) {
-  const int n = P.n;
-  const int gm = P.P_mgs / 32;
+__device__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
+                    unsigned long long epoch, double sqrt_eps) {
+  constexpr int L = limbs_of<R>::L;
+  const int N = P.N, n = P.n, Pm = P.P_mgs;
+  const long SA = (long)N * (n + 1);
+  const int gm = Pm / 32;
   const int gpc = kWarps / gm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gi = warp / gm;
   const Group g{gm, (warp % gm) * 32 + lane, 1 + gi};
-  const int G = team.nblocks * gpc;
-  const int me = team.block * gpc + gi;
+  const int nb = team.nblocks;
+  const int G = nb * gpc;
+  const int me = team.block + nb * gi;
+  if (me > n) return;  // owns no column
+  auto own = [&](int j) -> ColRef {
+    return colsm ? ColRef{colsm + (long)(j / nb) * 2 * L * N, (long)N} : ColRef{W.A + (long)j * N, SA};
+  };
+  if (colsm) {  // stage the owned columns (each thread its own rows: no sync needed)
+    for (int j = me; j <= n; j += G) {
+      const ColRef c = own(j);
+#pragma unroll
+      for (int r = 0; r < kMaxElems; ++r) {
+        const int i = g.p + r * Pm;
+        if (i < N) store_c<R>(c.p, c.S, i, ldcg_c<R>(W.A + (long)j * N, SA, i));
+      }
+    }
+  }
   int phase = 0;
   bool alive = true;
-  if (me > n) return;  // owns no column
   const int last_owned = me + ((n - me) / G) * G;
-  if (me == 0) alive = mgs_normalize<R, Team>(P, W, team, g, gi, sh, phase, 0, epoch, sqrt_eps);
+  // q_k travels through global memory (grid team, or no shared staging),
+  // else it is read from the owner CTA's shared memory (local or DSMEM)
+  const bool q_global = Team::kQInGlobal || colsm == nullptr;
+  if (me == 0) alive = mgs_normalize<R, Team>(P, W, team, g, gi, sh, phase, own(0), q_global, 0, epoch, sqrt_eps);
   for (int k = 0; k < n && alive && k < last_owned; ++k) {
-    if (k % G != me) {
-      if (g.p == 0) sh.ibcast[gi][phase] = wait_flag(W.flags + k, epoch, W.ctl) ? 1 : 0;
+    const bool mine = (k % G == me);
+    if (!mine) {
+      if (g.p == 0) sh.ibcast[gi][phase] = team.wait(W.flags, k, epoch);
       g.sync();
-      const int okw = sh.ibcast[gi][phase];
+      const int st = sh.ibcast[gi][phase];
       phase ^= 1;
-      if (!okw) return;
-      if (ld_acquire(W.ctl + CTL_RANK) == epoch) return;
+      if (st != 0) return;  // rank failure of column k, or abort
     }
-    // first owned column > k
-    int j = k + 1 + ((me - (k + 1)) % G + G) % G;
+    cplx<R> q[kMaxElems];
+    {
+      const double* qp;
+      long qS;
+      if (mine) {
+        const ColRef ck = own(k);
+        qp = ck.p;
+        qS = ck.S;
+      } else if (q_global) {
+        qp = W.A + (long)k * N;
+        qS = SA;
+      } else {
+        const double* loc = colsm + (long)(k / nb) * 2 * L * N;
+        qp = nb == 1 ? loc : cooperative_groups::this_cluster().map_shared_rank(const_cast<double*>(loc), k % nb);
+        qS = N;
+      }
+#pragma unroll
+      for (int r = 0; r < kMaxElems; ++r) {
+        const int i = g.p + r * Pm;
+        if (i < N) q[r] = (!mine && q_global) ? ldcg_c<R>(qp, qS, i) : load_c<R>(qp, qS, i);
+      }
+    }
+    int j = k + 1 + ((me - (k + 1)) % G + G) % G;  // first owned column > k
     for (; j <= n; j += G) {
-      mgs_project<R, Team>(P, W, g, gi, sh, phase, k, j);
+      const ColRef c = own(j);
+      mgs_project<R>(P, W, g, gi, sh, phase, q, c, k, j);
       if (j == k + 1 && j < n) {
-        if (!mgs_normalize<R, Team>(P, W, team, g, gi, sh, phase, j, epoch, sqrt_eps)) alive = false;
+        if (!mgs_normalize<R, Team>(P, W, team, g, gi, sh, phase, c, q_global, j, epoch, sqrt_eps)) alive = false;
       }
     }
   }
 }
 
 // Back substitution R dx = y, dx_k = (y_k - sum_{j>k} r_kj dx_j) * (1/r_kk),
-// column-oriented (one CTA); then u = max|dx| and x += dx.
+// column-oriented in one CTA with the next column of R prefetched one step
+// ahead (L2 latency off the dependency chain); then u = max|dx|, x += dx.
 template <class R>
 __device__ double backsub_update(const DevPlan& P, const Work& W, Smem<R>& sh) {
   const int n = P.n;
   const long SR = (long)n * (n + 1);
-  cplx<R> acc[kMaxRowsPerThread];
+  cplx<R> acc[kMaxRowsPerThread], cur[kMaxRowsPerThread], nxt[kMaxRowsPerThread];
+  R inv[kMaxRowsPerThread];
 #pragma unroll
   for (int r = 0; r < kMaxRowsPerThread; ++r) {
     const int i = threadIdx.x + r * kThreads;
-    if (i < n) acc[r] = load_c<R>(W.Rm, SR, (long)n * n + i);
+    if (i < n) {
+      acc[r] = load_c<R>(W.Rm, SR, (long)n * n + i);
+      inv[r] = load_r<R>(W.inv, n, i);
+      if (i < n - 1) cur[r] = load_c<R>(W.Rm, SR, (long)(n - 1) * n + i);
+    }
   }
   for (int j = n - 1; j >= 0; --j) {
     const int owner = j % kThreads, orow = j / kThreads;
     if ((int)threadIdx.x == owner) {
-      cplx<R> a;
 #pragma unroll
       for (int r = 0; r < kMaxRowsPerThread; ++r)
-        if (r == orow) a = acc[r];
-      const cplx<R> xj = c_scale(a, load_r<R>(W.inv, n, j));
+        if (r == orow) {
+          acc[r] = c_scale(acc[r], inv[r]);  // row j finished: acc now holds dx_j
+          sh.xbs[j & 1] = acc[r];
+        }
+    }
 #pragma unroll
-      for (int r = 0; r < kMaxRowsPerThread; ++r)
-        if (r == orow) acc[r] = xj;  // row j finished: acc now holds dx_j
-      sh.xbs[j & 1] = xj;
+    for (int r = 0; r < kMaxRowsPerThread; ++r) {
+      const int i = threadIdx.x + r * kThreads;
+      if (i < j - 1) nxt[r] = load_c<R>(W.Rm, SR, (long)(j - 1) * n + i);
     }
     __syncthreads();
     const cplx<R> xj = sh.xbs[j & 1];
 #pragma unroll
     for (int r = 0; r < kMaxRowsPerThread; ++r) {
       const int i = threadIdx.x + r * kThreads;
-      if (i < j) acc[r] = c_sub(acc[r], c_mul(load_c<R>(W.Rm, SR, (long)j * n + i), xj));
+      if (i < j) acc[r] = c_sub(acc[r], c_mul(cur[r], xj));
+      cur[r] = nxt[r];
     }
   }
   double u = 0.0;
@@ -635,18 +846,22 @@ struct NewtonOut {
 };
 
 template <class R, class Team>
-__device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh,
+__device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                             const pt_step_params& sp, double t, unsigned long long& epoch) {
   NewtonOut o{0, NW_ITERATION_BUDGET, 0, -1.0, -1.0, 0};
   const double sqrt_eps = kSqrtEps<R>();
   double last = bitsd(0x7ff0000000000000ull);
   const int tid = team.block * kThreads + threadIdx.x, nth = team.nblocks * kThreads;
+  PhaseClock pc(team.block == 0 && threadIdx.x == 0 && W.prof != nullptr);
   for (int it = 1; it <= sp.newton_max_iter; ++it) {
     o.iters = it;
+    if (pc.on) W.prof[PROF_ITERS] += 1;
     eval_monomials<R>(P, W, tid, nth);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    pc.lap(W.prof + PROF_MONO);
     eval_slots<R, Team>(P, W, team, sh, t);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    pc.lap(W.prof + PROF_SLOTS);
     double r = 0.0;
     for (int i = threadIdx.x; i < P.N; i += kThreads) r = nan_max(r, W.hmod[i]);
     r = block_nan_max(r, sh.red);
@@ -661,8 +876,10 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       return o;
     }
     ++epoch;
-    mgs<R, Team>(P, W, team, sh, epoch, sqrt_eps);
+    pc.lap(W.prof + PROF_SLOTS);
+    mgs<R, Team>(P, W, team, sh, colsm, epoch, sqrt_eps);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    pc.lap(W.prof + PROF_MGS);
     if (ld_acquire(W.ctl + CTL_RANK) == epoch) {
       o.kind = NW_LINEAR_SOLVE;
       return o;
@@ -672,6 +889,7 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       if (threadIdx.x == 0) W.scal[0] = u;
     }
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    pc.lap(W.prof + PROF_BACKSUB);
     const double u = *(volatile double*)(W.scal);
     ++o.solves;
     o.update = u;
@@ -695,7 +913,7 @@ struct TrackIO {
 };
 
 template <class R, class Team>
-__device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh,
+__device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                            const pt_step_params& sp, const TrackIO& io, unsigned long long epoch_base) {
   const int n = P.n;
   unsigned long long epoch = epoch_base;
@@ -704,7 +922,7 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
   if (leader)
     for (int i = threadIdx.x; i < n; i += kThreads) store_c<R>(W.x, n, i, load_c<R>(io.start, n, i));
   if (!team.sync(&sh.flag)) return;
-  NewtonOut o = newton<R, Team>(P, W, team, sh, sp, 0.0, epoch);
+  NewtonOut o = newton<R, Team>(P, W, team, sh, colsm, sp, 0.0, epoch);
   if (o.kind == NW_ABORT) return;
   st.start_iters = o.iters;
   st.newton_iters = o.iters;
@@ -735,9 +953,11 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
       }
       const double tsum = add64(tacc, dt);
       const double ttrial = tsum < 1.0 ? tsum : 1.0;
+      PhaseClock pc(leader && threadIdx.x == 0 && W.prof != nullptr);
       if (leader) predict<R>(P, W, H, ttrial);
       if (!team.sync(&sh.flag)) return;
-      o = newton<R, Team>(P, W, team, sh, sp, ttrial, epoch);
+      pc.lap(W.prof + PROF_PREDICT);
+      o = newton<R, Team>(P, W, team, sh, colsm, sp, ttrial, epoch);
       if (o.kind == NW_ABORT) return;
       st.newton_iters += o.iters;
       st.solves += o.solves;

@@ -122,6 +122,13 @@ PT_HD double bitsd(uint64_t b) {
 PT_HD uint64_t mag(double x) { return dbits(x) & 0x7fffffffffffffffull; }
 PT_HD bool finite(double x) { return (dbits(x) & 0x7ff0000000000000ull) != 0x7ff0000000000000ull; }
 PT_HD double fabs_(double x) { return bitsd(mag(x)); }
+PT_HD int clz32(unsigned x) {
+#if defined(__CUDA_ARCH__)
+  return __clz(x);
+#else
+  return x ? __builtin_clz(x) : 32;
+#endif
+}
 
 // Error-free transforms (multiprec.hpp:39-83).
 PT_HD double two_sum(double a, double b, double& e) {
@@ -340,23 +347,52 @@ PT_HDI qd qd_renorm5(double c0, double c1, double c2, double c3, double c4) {
 // insertion sort on |m| (descending, ties keep input order); any stable sort
 // yields the same permutation.  This is that insertion sort, fully unrolled
 // with static indices and an early exit, comparing magnitudes as integers.
+#ifndef PT_QD_SORT
+#define PT_QD_SORT 2
+#endif
 template <int K>
 PT_HD qd qd_distill(double (&m)[K]) {
+#if PT_QD_SORT == 2
+  // Insertion position by mask: all compares of the sorted prefix against v
+  // are independent; pos = 1 + index of the highest prefix entry with
+  // |m[j]| >= |v| (stable: ties stay in front); then an independent shift.
+  // Same permutation as the reference's insertion sort, constant depth per
+  // element instead of a chain as long as the move.
 #pragma unroll
   for (int i = 1; i < K; ++i) {
     const double v = m[i];
     const uint64_t av = mag(v);
+    if (mag(m[i - 1]) >= av) continue;  // already in place: the common case
+    unsigned keep = 0;  // bit j: m[j] stays in front of v
+#pragma unroll
+    for (int j = 0; j < i - 1; ++j) keep |= (mag(m[j]) >= av ? 1u : 0u) << j;
+    const int pos = 32 - clz32(keep);  // 0 when every prefix entry moves
+#pragma unroll
+    for (int j = i; j >= 1; --j) m[j] = (j > pos) ? m[j - 1] : (j == pos ? v : m[j]);
+    if (pos == 0) m[0] = v;
+  }
+#else
+#pragma unroll
+  for (int i = 1; i < K; ++i) {
+    const double v = m[i];
+    const uint64_t av = mag(v);
+    if (mag(m[i - 1]) >= av) continue;  // already in place: the common case
+    bool moving = true;
 #pragma unroll
     for (int j = i - 1; j >= 0; --j) {
-      if (mag(m[j]) < av) {
-        m[j + 1] = m[j];
-        if (j == 0) m[0] = v;
-      } else {
-        m[j + 1] = v;
-        break;
-      }
+#if defined(__CUDA_ARCH__) && PT_QD_SORT == 0
+      // leave once no lane of the warp still moves
+      if (!__any_sync(__activemask(), moving)) break;
+#elif !defined(__CUDA_ARCH__)
+      if (!moving) break;
+#endif
+      const bool c = moving && (mag(m[j]) < av);
+      m[j + 1] = c ? m[j] : (moving ? v : m[j + 1]);
+      moving = c;
     }
+    if (moving) m[0] = v;
   }
+#endif
   if (!finite(m[0])) return {{m[0], 0.0, 0.0, 0.0}};
 #pragma unroll
   for (int pass = 0; pass < 2; ++pass) {
@@ -375,12 +411,12 @@ PT_HD qd qd_distill(double (&m)[K]) {
 
 PT_HD qd r_from(double x, qd*) { return {{x, 0.0, 0.0, 0.0}}; }
 PT_HD qd r_neg(const qd& a) { return {{-a.c[0], -a.c[1], -a.c[2], -a.c[3]}}; }
-PT_QDOP qd r_add(const qd& a, const qd& b) {  // multiprec.hpp:290-293
+PT_QDOP qd r_add(qd a, qd b) {  // multiprec.hpp:290-293
   double m[8] = {a.c[0], a.c[1], a.c[2], a.c[3], b.c[0], b.c[1], b.c[2], b.c[3]};
   return qd_distill<8>(m);
 }
-PT_HD qd r_sub(const qd& a, const qd& b) { return r_add(a, r_neg(b)); }
-PT_QDOP qd r_mul(const qd& a, const qd& b) {  // multiprec.hpp:297-312
+PT_HD qd r_sub(qd a, qd b) { return r_add(a, r_neg(b)); }
+PT_QDOP qd r_mul(qd a, qd b) {  // multiprec.hpp:297-312
   double m[23];
   int k = 0;
 #pragma unroll
@@ -397,7 +433,7 @@ PT_QDOP qd r_mul(const qd& a, const qd& b) {  // multiprec.hpp:297-312
   m[22] = mul64(a.c[3], b.c[1]);
   return qd_distill<23>(m);
 }
-PT_QDOP qd r_mul_d(const qd& a, double b) {  // multiprec.hpp:314-323
+PT_QDOP qd r_mul_d(qd a, double b) {  // multiprec.hpp:314-323
   double m[8];
 #pragma unroll
   for (int i = 0; i <= 3; ++i) {
@@ -407,7 +443,7 @@ PT_QDOP qd r_mul_d(const qd& a, double b) {  // multiprec.hpp:314-323
   }
   return qd_distill<8>(m);
 }
-PT_QDOP qd r_div(const qd& a, const qd& b) {  // multiprec.hpp:327-337
+PT_QDOP qd r_div(qd a, qd b) {  // multiprec.hpp:327-337
   double q0 = div64(a.c[0], b.c[0]);
   if (!finite(q0)) return {{q0, 0.0, 0.0, 0.0}};
   double q[5];
@@ -422,7 +458,7 @@ PT_QDOP qd r_div(const qd& a, const qd& b) {  // multiprec.hpp:327-337
   }
   return qd_distill<5>(q);
 }
-PT_QDOP qd r_sqrt(const qd& a) {  // multiprec.hpp:364-372
+PT_QDOP qd r_sqrt(qd a) {  // multiprec.hpp:364-372
   if (a.c[0] == 0.0 && a.c[1] == 0.0 && a.c[2] == 0.0 && a.c[3] == 0.0) return {{0.0, 0.0, 0.0, 0.0}};
   if (a.c[0] < 0.0) return {{bitsd(0x7ff8000000000000ull), 0.0, 0.0, 0.0}};
   qd x{{div64(1.0, sqrt64(a.c[0])), 0.0, 0.0, 0.0}};
@@ -435,7 +471,7 @@ PT_HD double r_hi(const qd& a) { return a.c[0]; }
 PT_HD bool r_is_zero(const qd& a) { return a.c[0] == 0.0 && a.c[1] == 0.0 && a.c[2] == 0.0 && a.c[3] == 0.0; }
 PT_HD double r_limb(const qd& a, int l) { return a.c[l]; }
 PT_HD void r_set_limb(qd& a, int l, double v) { a.c[l] = v; }
-PT_QDOP qd qd_renormalize(const qd& a) {  // multiprec.hpp:283-286
+PT_QDOP qd qd_renormalize(qd a) {  // multiprec.hpp:283-286
   double m[4] = {a.c[0], a.c[1], a.c[2], a.c[3]};
   return qd_distill<4>(m);
 }

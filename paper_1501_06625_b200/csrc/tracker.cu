@@ -43,7 +43,7 @@ inline int limbs(pt_prec p) { return p == PT_D ? 1 : (p == PT_DD ? 2 : 4); }
 struct Layout {
   long x, hist, ws, A, Rm, inv, rmaxp, hmod, scal, dx;  // double offsets
   long dslice;
-  long flags, ctl;  // u64 offsets
+  long flags, ctl, prof;  // u64 offsets
   long uslice;
 };
 
@@ -71,6 +71,8 @@ Layout make_layout(int L, int n, int N, long ws_len) {
   u += (n + 1 + 31) & ~31L;
   o.ctl = u;
   u += 32;
+  o.prof = u;
+  u += 32;
   o.uslice = u;
   return o;
 }
@@ -91,6 +93,7 @@ __host__ __device__ inline Work carve(double* dbase, unsigned long long* ubase, 
   W.dx = d + o.dx;
   W.flags = u + o.flags;
   W.ctl = u + o.ctl;
+  W.prof = u + o.prof;
   return W;
 }
 
@@ -103,8 +106,24 @@ template <class R>
 __global__ void __launch_bounds__(kThreads, 1)
     k_track_grid(DevPlan P, Work W, pt_step_params sp, TrackIO io, unsigned long long epoch_base) {
   __shared__ Smem<R> sh;
-  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x};
-  track_path<R, GridTeam>(P, W, team, sh, sp, io, epoch_base);
+  extern __shared__ double dyn_smem[];
+  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
+  track_path<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
+}
+
+// One path on one thread-block cluster (launched with a cluster dimension
+// attribute, grid == cluster): barrier.cluster + DSMEM column exchange.
+template <class R>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_track_cluster(DevPlan P, Work W, pt_step_params sp, TrackIO io, unsigned long long epoch_base) {
+  __shared__ Smem<R> sh;
+  __shared__ uint32_t s_flags[kMaxCols];
+  extern __shared__ double dyn_smem[];
+  for (int i = threadIdx.x; i < kMaxCols; i += kThreads) s_flags[i] = 0;
+  const ClusterTeam team{W.ctl, (int)cluster_nranks(), (int)cluster_rank(), s_flags};
+  team.sync(&sh.flag);
+  track_path<R, ClusterTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
+  team.sync(&sh.flag);  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
 template <class R>
@@ -114,8 +133,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                   unsigned long long* queue, unsigned long long epoch_base) {
   __shared__ Smem<R> sh;
   __shared__ int s_path;
+  __shared__ uint32_t s_flags[kMaxCols];
+  extern __shared__ double dyn_smem[];
+  for (int i = threadIdx.x; i < kMaxCols; i += kThreads) s_flags[i] = 0;
   const Work W = carve(dbase, ubase, lay, blockIdx.x);
-  const BlockTeam team{W.ctl, 1, 0};
+  const BlockTeam team{W.ctl, 1, 0, s_flags};
   const long PS = 2L * limbs_of<R>::L * P.n;
   for (;;) {
     if (threadIdx.x == 0) s_path = (int)atomicAdd(queue, 1ull);
@@ -124,7 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (p >= n_paths) break;
     TrackIO io{starts + p * PS, ends + p * PS, stats + p, nullptr, 0, nullptr};
-    track_path<R, BlockTeam>(P, W, team, sh, sp, io, epoch_base + ((unsigned long long)p << 16));
+    track_path<R, BlockTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io,
+                             epoch_base + ((unsigned long long)p << 16));
   }
 }
 
@@ -132,7 +155,7 @@ template <class R>
 __global__ void __launch_bounds__(kThreads, 1)
     k_eval(DevPlan P, Work W, const double* x, double t, double* h, double* J, double* rmax) {
   __shared__ Smem<R> sh;
-  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x};
+  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
   const int n = P.n, N = P.N;
   if (team.block == 0)
     for (int i = threadIdx.x; i < n; i += kThreads) store_c<R>(W.x, n, i, load_c<R>(x, n, i));
@@ -158,8 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <class R>
 __global__ void __launch_bounds__(kThreads, 1) k_lstsq(DevPlan P, Work W, unsigned long long epoch, int* status) {
   __shared__ Smem<R> sh;
-  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x};
-  mgs<R, GridTeam>(P, W, team, sh, epoch, kSqrtEps<R>());
+  extern __shared__ double dyn_smem[];
+  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
+  mgs<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, epoch, kSqrtEps<R>());
   if (!team.sync(&sh.flag)) {
     if (team.block == 0 && threadIdx.x == 0) *status = PT_E_TIMEOUT;
     return;
@@ -247,6 +271,81 @@ __global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Latency microbenchmarks (one thread): dependent chains of the primitive and
+// emulated operations, in SM cycles per operation.
+__global__ void k_latency(double* out, double seed) {
+  const int T = 256;
+  long long c0, c1;
+  double a = seed, b = 1.0000001;
+  c0 = clock64();
+  for (int i = 0; i < T; ++i) a = __dadd_rn(a, b);
+  c1 = clock64();
+  out[0] = (double)(c1 - c0) / T;
+  out[10] = a;
+  dd x{seed, 0.0}, y{1.0000001, 1e-20};
+  c0 = clock64();
+  for (int i = 0; i < T; ++i) x = r_add(x, y);
+  c1 = clock64();
+  out[1] = (double)(c1 - c0) / T;
+  c0 = clock64();
+  for (int i = 0; i < T; ++i) x = r_mul(x, y);
+  c1 = clock64();
+  out[2] = (double)(c1 - c0) / T;
+  out[11] = x.hi;
+  qd q{{seed, 1e-17, 1e-34, 1e-51}}, w{{1.0000001, 1e-20, 1e-37, 1e-54}};
+  c0 = clock64();
+  for (int i = 0; i < T / 8; ++i) q = r_add(q, w);
+  c1 = clock64();
+  out[3] = (double)(c1 - c0) / (T / 8);
+  c0 = clock64();
+  for (int i = 0; i < T / 8; ++i) q = r_mul(q, w);
+  c1 = clock64();
+  out[4] = (double)(c1 - c0) / (T / 8);
+  out[12] = q.c[0];
+  cplx<dd> z{{seed, 0}, {0.5, 0}}, u{{0.9999, 1e-20}, {0.01, 0}};
+  c0 = clock64();
+  for (int i = 0; i < T; ++i) z = c_mul(z, u);
+  c1 = clock64();
+  out[5] = (double)(c1 - c0) / T;
+  out[13] = z.re.hi;
+  double h = seed;
+  c0 = clock64();
+  for (int i = 0; i < T; ++i) h = glibc_hypot(h, 0.5) * 0.5;
+  c1 = clock64();
+  out[6] = (double)(c1 - c0) / T;
+  out[14] = h;
+}
+
+// Grid barrier cost: every CTA crosses `iters` GridTeam barriers.
+__global__ void k_barrier(unsigned long long* ctl, int iters, double* out) {
+  __shared__ int flag;
+  const GridTeam team{ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
+  const unsigned long long t0 = gtimer();
+  for (int i = 0; i < iters; ++i)
+    if (!team.sync(&flag)) break;
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (double)(gtimer() - t0) / iters;
+}
+
+// Flag ping-pong between CTA 0 and CTA gridDim.x-1 (release/acquire through L2).
+__global__ void k_pingpong(unsigned long long* flags, int iters, double* out) {
+  if (threadIdx.x != 0) return;
+  const bool ping = blockIdx.x == 0, pong = blockIdx.x == gridDim.x - 1;
+  if (!ping && !pong) return;
+  const unsigned long long t0 = gtimer();
+  for (int i = 1; i <= iters; ++i) {
+    if (ping) {
+      st_release(flags, i);
+      while (ld_acquire(flags + 32) != (unsigned long long)i) {
+      }
+    } else {
+      while (ld_acquire(flags) != (unsigned long long)i) {
+      }
+      st_release(flags + 32, i);
+    }
+  }
+  if (ping) out[0] = (double)(gtimer() - t0) / iters / 2;  // one-way ns
+}
+
 // ---------------------------------------------------------------------------
 // plan object
 // ---------------------------------------------------------------------------
@@ -263,6 +362,11 @@ struct pt_plan {
   double* dwork = nullptr;  // single-path workspace (slice 0)
   unsigned long long* uwork = nullptr;
   int grid_blocks = 1;
+  size_t grid_dyn_smem = 0;   // dynamic smem of k_track_grid / k_eval
+  int engine = 0;             // 0 grid, 1 cluster (single path)
+  int cluster_size = 0;       // CTAs of the cluster engine (0: unavailable)
+  size_t cluster_dyn_smem = 0;
+  size_t batch_dyn_smem = 0;  // dynamic smem of k_track_batch
   // staging for the host-buffer API
   double* d_start = nullptr;
   double* d_end = nullptr;
@@ -309,6 +413,20 @@ int check_device(int device) {
   return PT_OK;
 }
 
+constexpr size_t kSmemBudget = 200 * 1024;  // dynamic smem ceiling per CTA (227 KB minus static)
+
+// bytes of owned MGS columns per CTA, 0 when they do not fit (global fallback)
+size_t mgs_smem_bytes(int L, int N, int n, int nblocks) {
+  const size_t cols = (size_t)(n + 1 + nblocks - 1) / nblocks;
+  const size_t bytes = cols * 2 * L * (size_t)N * 8;
+  return bytes <= kSmemBudget ? bytes : 0;
+}
+
+int set_dyn_smem(const void* fn, size_t bytes) {
+  PT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(bytes, 1)));
+  return PT_OK;
+}
+
 template <class R>
 int dispatch_grid_size(pt_plan* p, const void* fn) {
   int per_sm = 0, sms = 0;
@@ -323,6 +441,51 @@ int dispatch_grid_size(pt_plan* p, const void* fn) {
   want = std::max(want, (ntasks + kWarps - 1) / kWarps);
   want = std::max(want, (long)(p->n + 1 + gpc_mgs - 1) / gpc_mgs);
   p->grid_blocks = (int)std::min<long>(want, std::min(cap, sms));
+  p->grid_dyn_smem = mgs_smem_bytes(p->L, p->N, p->n, p->grid_blocks);
+  for (const void* f : {fn, (const void*)&k_eval<R>}) {
+    rc = set_dyn_smem(f, p->grid_dyn_smem);
+    if (rc) return rc;
+  }
+  int per_sm2 = 0;
+  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, fn, kThreads, p->grid_dyn_smem));
+  if (per_sm2 < 1) return fail(PT_E_INVAL, "tracker CTA does not fit on an SM");
+  return PT_OK;
+}
+
+// Largest cluster (<= 16 CTAs) the device can schedule for this kernel with
+// the MGS columns staged in shared memory.
+template <class R>
+int setup_cluster(pt_plan* p) {
+  const void* fn = (const void*)&k_track_cluster<R>;
+  PT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  p->cluster_size = 0;
+  for (int c : {16, 8, 4, 2}) {
+    const size_t dyn = mgs_smem_bytes(p->L, p->N, p->n, c);
+    if (dyn == 0) continue;
+    if (set_dyn_smem(fn, dyn)) return PT_E_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = dyn;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) == cudaSuccess && nclusters >= 1) {
+      p->cluster_size = c;
+      p->cluster_dyn_smem = dyn;
+      break;
+    }
+    cudaGetLastError();
+  }
+  // engine choice: systems whose MGS fits one cluster and whose evaluation is
+  // small enough that 16 SMs do not starve it run on the cluster engine
+  const double contributions = (double)p->n_ctr;
+  p->engine = (p->cluster_size >= 8 && p->n <= 192 && contributions <= 2e5) ? 1 : 0;
   return PT_OK;
 }
 
@@ -350,11 +513,31 @@ template <class R>
 void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
   Work W = carve(p->dwork, p->uwork, p->lay, 0);
   unsigned long long epoch = (++p->launches) << 40;
+  if (p->engine == 1) {
+    DevPlan dp = p->dp;
+    dp.mgs_smem = p->cluster_dyn_smem > 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p->cluster_size);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = p->cluster_dyn_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p->cluster_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    *err = cudaLaunchKernelEx(&cfg, k_track_cluster<R>, dp, W, sp, io, epoch);
+    return;
+  }
   DevPlan dp = p->dp;
+  dp.mgs_smem = p->grid_dyn_smem > 0;
   pt_step_params spc = sp;
   TrackIO ioc = io;
   void* args[] = {&dp, &W, &spc, &ioc, &epoch};
-  *err = cudaLaunchCooperativeKernel((const void*)&k_track_grid<R>, dim3(p->grid_blocks), dim3(kThreads), args, 0, s);
+  *err = cudaLaunchCooperativeKernel((const void*)&k_track_grid<R>, dim3(p->grid_blocks), dim3(kThreads), args,
+                                     p->grid_dyn_smem, s);
 }
 
 int validate_params(const pt_step_params* sp) {
@@ -415,7 +598,8 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     if (rc) return rc;
     const int L = limbs(prec);
     ptplan::HostPlan hp = ptplan::compile(g, f, L);
-    if (hp.n > kMaxRowsPerThread * kThreads) return fail(PT_E_INVAL, "n_vars > 1024 not supported");
+    if (hp.n > kMaxRowsPerThread * kThreads) return fail(PT_E_INVAL, "n_vars > 512 not supported");
+    if (hp.N > kMaxElems * 256) return fail(PT_E_INVAL, "n_eqs > 1024 not supported");
     PT_CUDA(cudaSetDevice(device));
     auto p = std::make_unique<pt_plan>();
     p->device = device;
@@ -491,6 +675,12 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
       default: rc = dispatch_grid_size<qd>(p.get(), grid_kernel<qd>()); break;
     }
     if (rc) return rc;
+    switch (prec) {
+      case PT_D: rc = setup_cluster<double>(p.get()); break;
+      case PT_DD: rc = setup_cluster<dd>(p.get()); break;
+      default: rc = setup_cluster<qd>(p.get()); break;
+    }
+    if (rc) return rc;
     *out = p.release();
     return PT_OK;
   });
@@ -519,8 +709,17 @@ int64_t pt_plan_info(const pt_plan* p, int32_t what) {
     case 5: return p->prec;
     case 6: return p->batch_blocks;
     case 7: return p->dp.ws_len;
+    case 8: return p->engine;
+    case 9: return p->cluster_size;
   }
   return -1;
+}
+
+int pt_plan_set_engine(pt_plan* p, int32_t engine) {
+  if (!p || engine < 0 || engine > 1) return fail(PT_E_INVAL, "engine must be 0 (grid) or 1 (cluster)");
+  if (engine == 1 && p->cluster_size == 0) return fail(PT_E_INVAL, "no schedulable cluster for this plan");
+  p->engine = engine;
+  return PT_OK;
 }
 
 int pt_plan_work(const pt_plan* p, int32_t kind, int32_t degree, double* out) {
@@ -564,6 +763,52 @@ int pt_fp64_peak(int device, double* instr_per_s, double* ms_out) {
   cudaFree(d);
   *instr_per_s = (double)blocks * threads * iters * kPeakChains / (best * 1e-3);
   if (ms_out) *ms_out = best;
+  return PT_OK;
+}
+
+int pt_plan_profile(pt_plan* p, double* out, int32_t reset) {
+  if (!p || !out) return PT_E_INVAL;
+  PT_CUDA(cudaSetDevice(p->device));
+  PT_CUDA(cudaStreamSynchronize(p->stream));
+  unsigned long long* prof = carve(p->dwork, p->uwork, p->lay, 0).prof;
+  unsigned long long h[kProfSlots];
+  PT_CUDA(cudaMemcpy(h, prof, sizeof h, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < kProfSlots; ++i) out[i] = (double)h[i];
+  if (reset) PT_CUDA(cudaMemset(prof, 0, sizeof h));
+  return PT_OK;
+}
+
+int pt_microbench(int device, int32_t what, double* out) {
+  if (!out) return PT_E_INVAL;
+  int rc = check_device(device);
+  if (rc) return rc;
+  PT_CUDA(cudaSetDevice(device));
+  double* d = dev_alloc<double>(32, &rc);
+  unsigned long long* u = dev_alloc<unsigned long long>(64, &rc);
+  if (rc) return rc;
+  PT_CUDA(cudaMemset(d, 0, 32 * 8));
+  PT_CUDA(cudaMemset(u, 0, 64 * 8));
+  cudaDeviceProp prop;
+  PT_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (what == 0) {
+    k_latency<<<1, 1>>>(d, 1.25);
+    PT_CUDA(cudaDeviceSynchronize());
+    k_latency<<<1, 1>>>(d, 1.25);
+  } else if (what == 1) {
+    int iters = 2000;
+    int blocks = prop.multiProcessorCount;
+    void* args[] = {&u, &iters, &d};
+    PT_CUDA(cudaLaunchCooperativeKernel((const void*)&k_barrier, dim3(blocks), dim3(kThreads), args, 0, 0));
+  } else if (what == 2) {
+    k_pingpong<<<prop.multiProcessorCount, 32>>>(u, 10000, d);
+  } else {
+    return fail(PT_E_INVAL, "unknown microbenchmark");
+  }
+  PT_CUDA(cudaGetLastError());
+  PT_CUDA(cudaDeviceSynchronize());
+  PT_CUDA(cudaMemcpy(out, d, 16 * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaFree(u);
   return PT_OK;
 }
 
@@ -630,8 +875,13 @@ static int ensure_batch(pt_plan* p) {
   const void* fn = p->prec == PT_D    ? (const void*)&k_track_batch<double>
                    : p->prec == PT_DD ? (const void*)&k_track_batch<dd>
                                       : (const void*)&k_track_batch<qd>;
-  int rc = occupancy_blocks(fn, p->device, &per_sm, &sms);
+  p->batch_dyn_smem = mgs_smem_bytes(p->L, p->N, p->n, 1);
+  int rc = set_dyn_smem(fn, p->batch_dyn_smem);
   if (rc) return rc;
+  cudaDeviceProp prop;
+  PT_CUDA(cudaGetDeviceProperties(&prop, p->device));
+  sms = prop.multiProcessorCount;
+  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, p->batch_dyn_smem));
   p->batch_blocks = std::max(1, per_sm) * sms;
   p->bwork = dev_alloc<double>((size_t)p->lay.dslice * p->batch_blocks, &rc);
   if (rc) return rc;
@@ -657,17 +907,19 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 8, s));
   const unsigned long long epoch = (++p->launches) << 40;
   const int blocks = std::min(p->batch_blocks, n_paths);
+  DevPlan bdp = p->dp;
+  bdp.mgs_smem = p->batch_dyn_smem > 0;
   switch (p->prec) {
     case PT_D:
-      k_track_batch<double><<<blocks, kThreads, 0, s>>>(p->dp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
+      k_track_batch<double><<<blocks, kThreads, p->batch_dyn_smem, s>>>(bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
                                                         n_paths, p->d_queue, epoch);
       break;
     case PT_DD:
-      k_track_batch<dd><<<blocks, kThreads, 0, s>>>(p->dp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
+      k_track_batch<dd><<<blocks, kThreads, p->batch_dyn_smem, s>>>(bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
                                                     n_paths, p->d_queue, epoch);
       break;
     default:
-      k_track_batch<qd><<<blocks, kThreads, 0, s>>>(p->dp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
+      k_track_batch<qd><<<blocks, kThreads, p->batch_dyn_smem, s>>>(bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
                                                     n_paths, p->d_queue, epoch);
       break;
   }
@@ -716,9 +968,10 @@ int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J
   PT_CUDA(cudaMemcpy(dx, x, (size_t)2 * L * n * 8, cudaMemcpyHostToDevice));
   Work W = carve(p->dwork, p->uwork, p->lay, 0);
   DevPlan dp = p->dp;
+  dp.mgs_smem = 0;
   void* args[] = {&dp, &W, &dx, &t, &dh, &dJ, &dr};
   const void* fn = p->prec == PT_D ? (const void*)&k_eval<double> : p->prec == PT_DD ? (const void*)&k_eval<dd> : (const void*)&k_eval<qd>;
-  PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, 0, p->stream));
+  PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, p->grid_dyn_smem, p->stream));
   PT_CUDA(cudaStreamSynchronize(p->stream));
   if (h) PT_CUDA(cudaMemcpy(h, dh, (size_t)2 * L * N * 8, cudaMemcpyDeviceToHost));
   if (J) PT_CUDA(cudaMemcpy(J, dJ, (size_t)2 * L * N * n * 8, cudaMemcpyDeviceToHost));
@@ -732,7 +985,8 @@ int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J
 
 int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, const double* b, double* x) {
   return guarded([&]() -> int {
-    if (!A || !b || !x || n < 1 || N < n || n > kMaxRowsPerThread * kThreads) return fail(PT_E_INVAL, "bad lstsq arguments");
+    if (!A || !b || !x || n < 1 || N < n || n > kMaxRowsPerThread * kThreads || N > kMaxElems * 256)
+      return fail(PT_E_INVAL, "bad lstsq arguments");
     int rc = check_device(device);
     if (rc) return rc;
     PT_CUDA(cudaSetDevice(device));
@@ -764,9 +1018,13 @@ int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, co
     rc = occupancy_blocks(fn, device, &per_sm, &sms);
     if (rc) return rc;
     int blocks = std::min(std::min(sms, std::max(1, per_sm) * sms), std::max(1, (n + 1 + gpc - 1) / gpc));
+    const size_t dyn = mgs_smem_bytes(L, N, n, blocks);
+    rc = set_dyn_smem(fn, dyn);
+    if (rc) return rc;
+    dp.mgs_smem = dyn > 0;
     unsigned long long epoch = 1;
     void* args[] = {&dp, &W, &epoch, &dstat};
-    PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), args, 0, 0));
+    PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), args, dyn, 0));
     PT_CUDA(cudaDeviceSynchronize());
     int st = 0;
     PT_CUDA(cudaMemcpy(&st, dstat, 4, cudaMemcpyDeviceToHost));

@@ -285,6 +285,14 @@ class Homotopy:
     def info(self, what: int) -> int:
         return int(nat.lib.pt_plan_info(self._plan, what))
 
+    @property
+    def engine(self) -> str:
+        return ("grid", "cluster")[self.info(8)]
+
+    def set_engine(self, engine: str) -> None:
+        """Force the single-path engine ("grid" or "cluster"); results are bit-identical."""
+        nat.check(nat.lib.pt_plan_set_engine(self._plan, {"grid": 0, "cluster": 1}[engine]))
+
     def track_path(self, start: np.ndarray, params: Optional[StepControlParams] = None,
                    trace: bool = False) -> TrackOutcome:
         """track_path (SPEC.md:466-474)."""

@@ -83,13 +83,25 @@ def _compare_track(w, out, end_ref, st_ref, tr_ref):
     assert_bits_equal(out.end, end_ref, "end point")
 
 
+_REF_TRACKS = {}
+
+
+def _ref_track(oracle, name, prec):
+    key = (name, prec)
+    if key not in _REF_TRACKS:
+        w = W.by_name(name, prec)
+        cap = w.params.max_steps + 2
+        _REF_TRACKS[key] = (w, oracle.track_path(int(prec), w.g, w.f, w.gamma, w.k, w.start, w.params, cap))
+    return _REF_TRACKS[key]
+
+
+@pytest.mark.parametrize("engine", ["grid", "cluster"])
 @pytest.mark.parametrize("name,prec", [("cyclic16", PM.DD), ("cyclic16", PM.D), ("chandra64", PM.D),
                                        ("chandra64", PM.DD), ("chandra64", PM.QD)])
-def test_track_path_bitwise(gpu, oracle, name, prec):
-    w = W.by_name(name, prec)
-    cap = w.params.max_steps + 2
-    end_ref, st_ref, tr_ref = oracle.track_path(int(prec), w.g, w.f, w.gamma, w.k, w.start, w.params, cap)
+def test_track_path_bitwise(gpu, oracle, name, prec, engine):
+    w, (end_ref, st_ref, tr_ref) = _ref_track(oracle, name, prec)
     hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)
+    hom.set_engine(engine)
     out = hom.track_path(w.start, w.params, trace=True)
     _compare_track(w, out, end_ref, st_ref, tr_ref)
     if name == "chandra64":
