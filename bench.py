@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--prec", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--max-steps", type=int, default=None,
+                    help="track only a prefix of the path (per-step timing of huge configs)")
     return ap.parse_args()
 
 
@@ -68,6 +70,13 @@ def workload(args):
     if args.workload == "batch32":
         return W.batch(prec=(prec if prec is not None else PrecisionMode.DD))
     raise SystemExit(f"unknown workload {args.workload}")
+
+
+def apply_overrides(args, w):
+    if args.max_steps is not None:
+        w.params.max_steps = args.max_steps
+        w.name += f"-prefix{args.max_steps}"
+    return w
 
 
 def config(args, w, world):
@@ -199,7 +208,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    w = workload(args)
+    w = apply_overrides(args, workload(args))
     per_step = max(args.cpu_seconds / max(args.steps, 1), 0.5)
     vals = []
     for _ in range(args.warmup):
@@ -229,7 +238,7 @@ def run_ours(args):
     import paper_1501_06625_b200 as pt
     from paper_1501_06625_b200 import _native as nat
 
-    w = workload(args)
+    w = apply_overrides(args, workload(args))
     L, n = w.prec.limbs, w.n
     batch = args.workload == "batch32"
     hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=device)
@@ -335,7 +344,9 @@ def run_ours(args):
             "config": config(args, w, world),
             "sec_per_path": t_dev_max / args.steps / (npaths if batch else 1),
             "path": {"success": ok, "steps": stats_list[0].steps, "newton_iters": stats_list[0].newton_iters,
-                     "solves": stats_list[0].solves, "grid_ctas": hom.info(4)},
+                     "solves": stats_list[0].solves, "grid_ctas": hom.info(4), "engine": hom.engine,
+                     "cluster_ctas": hom.info(9), "paths_ok": int(sum(s.status == 0 for s in stats_list)),
+                     "paths": len(stats_list)},
             "e2e": {"value": e2e_value, "unit": "paths/s",
                     "h2d_bytes_per_step": int(h_start.numel() * 8),
                     "d2h_bytes_per_step": int(h_end.numel() * 8 + C.sizeof(nat.PathStats) * npaths),

@@ -163,6 +163,11 @@ int pt_microbench(int device, int32_t what, double* out);
  * iterations (count); reset != 0 clears them. */
 int pt_plan_profile(pt_plan* plan, double* out, int32_t reset);
 
+/* MGS timeline of the last single-path launch (debugging aid): for column j,
+ * out[3j..3j+2] = globaltimer ns when q_{j-1} reached the owner of column j,
+ * after its projection, after q_j was published. */
+int pt_plan_mgs_timeline(pt_plan* plan, double* out, int32_t count);
+
 /* Enable a per-trial trace of up to `capacity` events (0 disables). */
 int pt_plan_set_trace(pt_plan* plan, int32_t capacity);
 /* Copy the trace of the last pt_track_path call; *count = events recorded. */

@@ -42,7 +42,8 @@ enum { NW_OK = 0, NW_RESIDUAL_INCREASE = 1, NW_ITERATION_BUDGET = 2, NW_LINEAR_S
 
 struct DevPlan {
   int n, N, M;
-  int P_mgs;
+  int P_mgs;   // canonical width of the MGS sums
+  int mgs_gw;  // warps per MGS group (>= P_mgs/32; one element per thread when N <= 256)
   const int32_t* mono_size;
   const int32_t* mono_vbeg;
   const int32_t* mono_out;
@@ -51,7 +52,7 @@ struct DevPlan {
   const int32_t* mono_exp;
   long ws_len;
   const ptplan::SlotTask* tasks;
-  int class_beg[5];
+  int class_beg[6];
   const int32_t* ctr_coef;
   const int32_t* ctr_ws;
   const double* coef;
@@ -80,6 +81,8 @@ struct Work {
 
 // Phase timers: block 0 / thread 0 accumulates globaltimer deltas.
 enum { PROF_MONO = 0, PROF_SLOTS = 1, PROF_MGS = 2, PROF_BACKSUB = 3, PROF_PREDICT = 4, PROF_ITERS = 5, kProfSlots = 8 };
+// W.prof[kProfSlots + 6*j + {0..5}]: owner of column j, last MGS of the launch (debugging aid):
+// globaltimer + clock64 when q_{j-1} was seen, clock64 after q loaded / projected / published, globaltimer at publish
 struct PhaseClock {
   unsigned long long t;
   bool on;
@@ -110,6 +113,11 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -132,8 +140,13 @@ __device__ __forceinline__ int wait_flag(const unsigned long long* flag, unsigne
   const unsigned long long t0 = gtimer();
   unsigned int spins = 0;
   for (;;) {
-    const unsigned long long v = ld_acquire(flag);
-    if ((v >> 1) == epoch) return (int)(v & 1ull);
+    // relaxed polling (an acquire load would invalidate L1 on every poll),
+    // one acquire fence once the flag is seen
+    const unsigned long long v = ld_relaxed(flag);
+    if ((v >> 1) == epoch) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      return (int)(v & 1ull);
+    }
     if ((++spins & 255u) == 0) {
       if (ld_acquire(ctl + CTL_ABORT)) return -1;
       if ((double)(gtimer() - t0) > kTimeoutNs) {
@@ -195,7 +208,7 @@ struct GridTeam {
       } else {
         const unsigned long long t0 = gtimer();
         unsigned int spins = 0;
-        while (ld_acquire(ctl + CTL_BAR_GEN) == gen) {
+        while (ld_relaxed(ctl + CTL_BAR_GEN) == gen) {
           if ((++spins & 255u) == 0) {
             if (ld_acquire(ctl + CTL_ABORT)) {
               abort = 1;
@@ -240,7 +253,10 @@ struct ClusterTeam {
   __device__ void publish(unsigned long long*, int k, unsigned long long epoch, int fail) const {
     const uint32_t v = ((uint32_t)(epoch & 0x7fffffffull) << 1) | (uint32_t)fail;
     const uint32_t local = smem_u32(sflags + k);
-    for (int r = 0; r < nblocks; ++r) st_release_cluster_u32(mapa_u32(local, (uint32_t)r), v);
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");  // one release fence, then relaxed remote flag stores
+    for (int r = 0; r < nblocks; ++r)
+      asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;" ::"r"(mapa_u32(local, (uint32_t)r)), "r"(v)
+                   : "memory");
   }
   __device__ int wait(const unsigned long long*, int k, unsigned long long epoch) const {
     const uint32_t want = (uint32_t)(epoch & 0x7fffffffull);
@@ -248,8 +264,13 @@ struct ClusterTeam {
     const unsigned long long t0 = gtimer();
     unsigned int spins = 0;
     for (;;) {
-      const uint32_t v = ld_acquire_cluster_u32(a);
-      if ((v >> 1) == want) return (int)(v & 1u);
+      uint32_t v;
+      asm volatile("ld.relaxed.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+      if ((v >> 1) == want) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        return (int)(v & 1u);
+      }
+      __nanosleep(32);
       if ((++spins & 1023u) == 0 && (double)(gtimer() - t0) > kTimeoutNs) {
         atomicExch(ctl + CTL_ABORT, 1ull);
         __trap();  // hardware cluster barriers cannot be abandoned: kill the launch instead of hanging
@@ -326,7 +347,7 @@ struct Group {
 // Canonical tree over the partials held by threads p < min(Pw, K); the result
 // is valid in thread p == 0.  sm: Pw scratch entries owned by this group.
 template <class T>
-__device__ T group_tree(T acc, const Group& g, int Pw, int K, T* sm) {
+__device__ __forceinline__ T group_tree(T acc, const Group& g, int Pw, int K, T* sm) {
   if (Pw > 32) {
     if (g.p < Pw && g.p < K) sm[g.p] = acc;
     g.sync();
@@ -336,12 +357,15 @@ __device__ T group_tree(T acc, const Group& g, int Pw, int K, T* sm) {
     }
     if (g.p < 32 && g.p < K) acc = sm[g.p];
   }
-  if (g.p < 32) {
-#pragma unroll 1
-    for (int off = 16; off >= 1; off >>= 1) {
-      T other = shfl_down_r(acc, off);
-      if (g.p < off && g.p + off < K) acc = add_v(acc, other);
-    }
+  // Warp levels: every warp of the group runs them (only warp 0's lanes
+  // p < off, p + off < K add), so the shuffles are in provably converged
+  // code -- under a lane-dependent branch nvcc falls back to the slow
+  // WARPSYNC.COLLECTIVE shuffle emulation.
+  __syncwarp();
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    T other = shfl_down_r(acc, off);
+    if (g.p < off && g.p + off < K) acc = add_v(acc, other);
   }
   return acc;
 }
@@ -381,6 +405,7 @@ struct Smem {
   int ibcast[kWarps][2];
   cplx<R> xbs[2];           // back-substitution broadcast
   double red[kWarps];
+  double pmax[kMaxCols];    // MGS prefix max of r_kk (cluster / block teams)
   int flag;
 };
 
@@ -400,7 +425,7 @@ __device__ void weights(const DevPlan& P, double t, cplx<R>& wS, R& wT) {
 // Prefix products F[j] are parked in the slot of partial j+1 and consumed by
 // the backward sweep, so the workspace is the only scratch.
 template <class R>
-__device__ void eval_monomials(const DevPlan& P, const Work& W, int tid, int nthreads) {
+__device__ __noinline__ void eval_monomials(const DevPlan& P, const Work& W, int tid, int nthreads) {
   const long S = P.ws_len;
   for (int q = tid; q < P.M; q += nthreads) {
     const int m = P.mono_size[q];
@@ -455,7 +480,7 @@ __device__ void eval_monomials(const DevPlan& P, const Work& W, int tid, int nth
 
 // Canonical sum of one contribution list by a group; valid at g.p == 0.
 template <class R>
-__device__ cplx<R> slot_sum(const DevPlan& P, const Work& W, const Group& g, int beg, int K, cplx<R>* sm) {
+__device__ __forceinline__ cplx<R> slot_sum(const DevPlan& P, const Work& W, const Group& g, int beg, int K, cplx<R>* sm) {
   const int Pw = width_eval_d(K);
   cplx<R> acc = c_zero<R>();
   if (g.p < Pw && g.p < K) {
@@ -470,13 +495,74 @@ __device__ cplx<R> slot_sum(const DevPlan& P, const Work& W, const Group& g, int
   return group_tree(acc, g, Pw, K, sm);
 }
 
+// Width-32 canonical sum of K <= KMAX contributions evaluated by one lane:
+// partial p = c[p]; levels off = 4, 2, 1 (the only ones with p + off < K).
+template <class R, int KMAX>
+__device__ __forceinline__ cplx<R> lane_sum(const DevPlan& P, const Work& W, int beg, int K) {
+  cplx<R> part[KMAX];
+#pragma unroll
+  for (int r = 0; r < KMAX; ++r) {
+    if (r < K) {
+      const int ci = P.ctr_coef[beg + r];
+      const int wi = P.ctr_ws[beg + r];
+      const cplx<R> c = load_c<R>(P.coef, P.n_coef, ci);
+      part[r] = wi < 0 ? c : c_mul(c, load_c<R>(W.ws, P.ws_len, wi));
+    }
+  }
+#pragma unroll
+  for (int off = KMAX / 2; off >= 1; off >>= 1) {
+#pragma unroll
+    for (int p = 0; p < off; ++p)
+      if (p + off < K) part[p] = c_add(part[p], part[p + off]);
+  }
+  return part[0];
+}
+
+template <class R>
+__device__ __forceinline__ void slot_store(const DevPlan& P, const Work& W, const ptplan::SlotTask& tk,
+                                           const cplx<R>& Sg, const cplx<R>& Sf, bool have_f, const cplx<R>& wS,
+                                           const R& wT) {
+  const long SA = (long)P.N * (P.n + 1);
+  const bool have_g = tk.g_cnt > 0;
+  cplx<R> h = c_zero<R>();
+  if (have_g || have_f) {
+    const cplx<R> zero = c_zero<R>();
+    h = c_add(c_mul(wS, have_g ? Sg : zero), c_scale(have_f ? Sf : zero, wT));
+  }
+  if (tk.col == P.n) {
+    store_c<R>(W.A, SA, (long)P.n * P.N + tk.row, c_neg(h));
+    W.hmod[tk.row] = c_mod_double(h);
+  } else {
+    store_c<R>(W.A, SA, (long)tk.col * P.N + tk.row, h);
+  }
+}
+
 template <class R, class Team>
-__device__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double t) {
+__device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double t) {
   cplx<R> wS;
   R wT;
   weights<R>(P, t, wS, wT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long SA = (long)P.N * (P.n + 1);
+  {  // lane tasks: one small slot per lane
+    constexpr int KM = limbs_of<R>::L == 4 ? 4 : 8;
+    const int beg = P.class_beg[0], end = P.class_beg[1];
+    const int nth = team.nblocks * kThreads;
+    for (int ti = beg + team.block * kThreads + threadIdx.x; ti < end; ti += nth) {
+      const ptplan::SlotTask tk = P.tasks[ti];
+      cplx<R> Sg = c_zero<R>(), Sf;
+      if (tk.g_cnt > 0) Sg = lane_sum<R, KM>(P, W, tk.g_beg, tk.g_cnt);
+      bool have_f;
+      if (tk.f_cnt < 0) {
+        Sf = Sg;
+        have_f = tk.g_cnt > 0;
+      } else {
+        Sf = c_zero<R>();
+        if (tk.f_cnt > 0) Sf = lane_sum<R, KM>(P, W, tk.f_beg, tk.f_cnt);
+        have_f = tk.f_cnt > 0;
+      }
+      slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);
+    }
+  }
   for (int c = 0; c < 4; ++c) {
     const int gw = 8 >> c;
     const int gpc = kWarps / gw;
@@ -484,7 +570,7 @@ __device__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Sm
     Group g{gw, (warp % gw) * 32 + lane, 1 + gi};
     cplx<R>* sm = sh.tree + gi * 32 * gw;
     const int ngroups = team.nblocks * gpc;
-    const int beg = P.class_beg[c], end = P.class_beg[c + 1];
+    const int beg = P.class_beg[c + 1], end = P.class_beg[c + 2];
     for (int ti = beg + team.block * gpc + gi; ti < end; ti += ngroups) {
       const ptplan::SlotTask tk = P.tasks[ti];
       const cplx<R> Sg = slot_sum<R>(P, W, g, tk.g_beg, tk.g_cnt, sm);
@@ -497,20 +583,7 @@ __device__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Sm
         Sf = slot_sum<R>(P, W, g, tk.f_beg, tk.f_cnt, sm);
         have_f = tk.f_cnt > 0;
       }
-      if (g.p == 0) {
-        const bool have_g = tk.g_cnt > 0;
-        cplx<R> h = c_zero<R>();
-        if (have_g || have_f) {
-          const cplx<R> zero = c_zero<R>();
-          h = c_add(c_mul(wS, have_g ? Sg : zero), c_scale(have_f ? Sf : zero, wT));
-        }
-        if (tk.col == P.n) {
-          store_c<R>(W.A, SA, (long)P.n * P.N + tk.row, c_neg(h));
-          W.hmod[tk.row] = c_mod_double(h);
-        } else {
-          store_c<R>(W.A, SA, (long)tk.col * P.N + tk.row, h);
-        }
-      }
+      if (g.p == 0) slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);
       g.sync();  // protect the group scratch before the next task
     }
   }
@@ -520,7 +593,7 @@ __device__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Sm
 // (2) MGS least squares on [J | -h]
 // ---------------------------------------------------------------------------
 template <class R>
-__device__ R group_bcast_r(const Group& g, int gi, R v, Smem<R>& sh, int& phase) {
+__device__ __forceinline__ R group_bcast_r(const Group& g, int gi, R v, Smem<R>& sh, int& phase) {
   if (g.p == 0) sh.rbcast[gi][phase] = v;
   g.sync();
   R r = sh.rbcast[gi][phase];
@@ -528,7 +601,7 @@ __device__ R group_bcast_r(const Group& g, int gi, R v, Smem<R>& sh, int& phase)
   return r;
 }
 template <class R>
-__device__ cplx<R> group_bcast_c(const Group& g, int gi, const cplx<R>& v, Smem<R>& sh, int& phase) {
+__device__ __forceinline__ cplx<R> group_bcast_c(const Group& g, int gi, const cplx<R>& v, Smem<R>& sh, int& phase) {
   if (g.p == 0) sh.bcast[gi][phase] = v;
   g.sync();
   cplx<R> r = sh.bcast[gi][phase];
@@ -555,107 +628,175 @@ __device__ __forceinline__ cplx<R> ldcg_c(const double* p, long S, long i) {
   return v;
 }
 
+// complex entry i of an SoA vector in another CTA's shared memory (DSMEM);
+// base = shared::cluster address of element 0
+template <class R>
+__device__ __forceinline__ cplx<R> ldsc_c(uint32_t base, long S, long i) {
+  constexpr int L = limbs_of<R>::L;
+  cplx<R> v;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    double a, b;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(a) : "r"(base + (uint32_t)(8 * (l * S + i))));
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(b) : "r"(base + (uint32_t)(8 * ((L + l) * S + i))));
+    r_set_limb(v.re, l, a);
+    r_set_limb(v.im, l, b);
+  }
+  return v;
+}
+
 constexpr int kMaxElems = 4;  // ceil(N / P_mgs) <= 4  (N <= 1024)
 
-// Normalise column k (already projected against q_0..q_{k-1}), write q_k to
-// the global matrix and publish it.  Returns false on rank deficiency (the
-// flag is still published so nobody hangs).
-template <class R, class Team>
-__device__ bool mgs_normalize(const DevPlan& P, const Work& W, const Team& team, const Group& g, int gi, Smem<R>& sh,
-                              int& phase, const ColRef& c, bool q_to_global, int k, unsigned long long epoch,
-                              double sqrt_eps) {
-  const int N = P.N, Pm = P.P_mgs;
+// Where one owned column keeps its data while the factorisation runs.
+struct OwnedCol {
+  ColRef a;       // the column itself (becomes q_j)
+  ColRef r;       // R column j: r_kj at index k (k <= j)
+  double* inv;    // 1/r_jj (L limbs, stride 1 in shared memory / n in global)
+  long inv_S;
+  int inv_i;
+};
+
+// Shared-memory layout of the MGS staging area of one CTA (dynamic smem):
+// [cols][2L][N] columns, then [cols][2L][n+1] R columns, then [cols][L] inverses.
+__host__ __device__ inline size_t mgs_stage_doubles(int L, int N, int n, int cols) {
+  return (size_t)cols * (2 * L * (size_t)N + 2 * L * (size_t)(n + 1) + L);
+}
+
+// Normalise column j (already projected against q_0..q_{j-1}) and publish it.
+// prev = max_{k<j} r_kk (binary64).  Returns false on rank deficiency (the
+// flag is still published, with the failure bit, so nobody hangs).
+// S: the owned column, its R column and inverse live in this CTA's shared
+// memory (tell nvcc, so it emits LDS/STS instead of generic loads).
+template <bool S>
+__device__ __forceinline__ void assume_shared(const OwnedCol& c) {
+  if constexpr (S) {
+    if (!__isShared(c.a.p) || !__isShared(c.r.p) || !__isShared(c.inv)) __builtin_unreachable();
+  }
+}
+
+// Canonical width-Pm sum of the group's element values v[r] (element
+// i = g.p + r*32*gw).  With 32*gw == Pm thread p owns partial p and adds its
+// elements in order; with 32*gw > Pm (then every thread holds at most one
+// element and N > Pm) element p + m*Pm is held by thread p + m*Pm and handed
+// to thread p through shared memory, so partial p = c[p] + c[p+Pm] + ... in
+// the same order either way.
+template <class T>
+__device__ __forceinline__ T mgs_reduce(const T* v, const Group& g, int Pm, int N, T* sm) {
+  const int TT = 32 * g.gw;
+  T acc = v[0];
+  if (TT == Pm) {
+#pragma unroll
+    for (int r = 1; r < kMaxElems; ++r)
+      if (g.p + r * Pm < N) acc = add_v(acc, v[r]);
+  } else {
+    if (g.p >= Pm && g.p < N) sm[g.p - Pm] = v[0];
+    g.sync();
+    if (g.p < Pm)
+      for (int m = 1; g.p + m * Pm < N; ++m) acc = add_v(acc, sm[(m - 1) * Pm + g.p]);
+  }
+  return group_tree(acc, g, Pm, N, sm);
+}
+
+template <class R, class Team, bool S>
+__device__ __forceinline__ bool mgs_normalize(const DevPlan& P, const Work& W, const Team& team, const Group& g, int gi, Smem<R>& sh,
+                              int& phase, const OwnedCol& c, bool q_to_global, double* pmax_sm, int j, double prev,
+                              unsigned long long epoch, double sqrt_eps) {
+  assume_shared<S>(c);
+  const int N = P.N, Pm = P.P_mgs, TT = 32 * g.gw;
   const long SA = (long)N * (P.n + 1);
-  R acc = rconst<R>(0.0);
+  R v[kMaxElems];
 #pragma unroll
   for (int r = 0; r < kMaxElems; ++r) {
-    const int i = g.p + r * Pm;
-    if (i < N) {
-      const R v = c_norm_sqr(load_c<R>(c.p, c.S, i));
-      acc = (r == 0) ? v : r_add(acc, v);
-    }
+    const int i = g.p + r * TT;
+    v[r] = i < N ? c_norm_sqr(load_c<R>(c.a.p, c.a.S, i)) : rconst<R>(0.0);
   }
   R* rsm = reinterpret_cast<R*>(sh.tree + (gi * 32 * g.gw));
-  const R nrm2 = group_tree(acc, g, Pm, N, rsm);
+  const R nrm2 = mgs_reduce(v, g, Pm, N, rsm);
   int ok = 0;
   R inv = rconst<R>(0.0);
   if (g.p == 0) {
-    const R rkk = r_sqrt(nrm2);
-    const double d = r_hi(rkk);
-    const double prev = k > 0 ? __ldcg(W.rmaxp + k - 1) : 0.0;
+    const R rjj = r_sqrt(nrm2);
+    const double d = r_hi(rjj);
     const double mx = d > prev ? d : prev;
     ok = d > sqrt_eps * mx;
-    W.rmaxp[k] = mx;
+    if (pmax_sm)
+      pmax_sm[j] = mx;
+    else
+      W.rmaxp[j] = mx;
     if (ok) {
-      inv = r_div(rconst<R>(1.0), rkk);
-      store_r<R>(W.inv, P.n, k, inv);
-      store_c<R>(W.Rm, (long)P.n * (P.n + 1), (long)k * P.n + k, cplx<R>{rkk, rconst<R>(0.0)});
+      inv = r_div(rconst<R>(1.0), rjj);
+      store_r<R>(c.inv, c.inv_S, c.inv_i, inv);
+      store_c<R>(c.r.p, c.r.S, j, cplx<R>{rjj, rconst<R>(0.0)});
     }
     sh.ibcast[gi][phase] = ok;
   }
   inv = group_bcast_r<R>(g, gi, inv, sh, phase);
   ok = sh.ibcast[gi][phase ^ 1];
   if (ok) {
-    double* gk = W.A + (long)k * N;
+    double* gj = W.A + (long)j * N;
 #pragma unroll
     for (int r = 0; r < kMaxElems; ++r) {
-      const int i = g.p + r * Pm;
+      const int i = g.p + r * TT;
       if (i < N) {
-        const cplx<R> q = c_scale(load_c<R>(c.p, c.S, i), inv);
-        store_c<R>(c.p, c.S, i, q);
-        if (q_to_global && c.p != gk) store_c<R>(gk, SA, i, q);
+        const cplx<R> q = c_scale(load_c<R>(c.a.p, c.a.S, i), inv);
+        store_c<R>(c.a.p, c.a.S, i, q);
+        if (q_to_global && c.a.p != gj) store_c<R>(gj, SA, i, q);
       }
     }
   }
   g.sync();
   if (g.p == 0) {
     if (!ok) atomicExch(W.ctl + CTL_RANK, epoch);
-    team.publish(W.flags, k, epoch, !ok);  // release: cumulative over the group's writes (bar.sync above)
+    team.publish(W.flags, j, epoch, !ok);  // release: cumulative over the group's writes (bar.sync above)
   }
   return ok != 0;
 }
 
 // r_kj = q_k^H a_j (canonical width P_mgs), a_j -= r_kj q_k.  q: this thread's
 // elements of q_k (rows p + r*P_mgs).
-template <class R>
-__device__ void mgs_project(const DevPlan& P, const Work& W, const Group& g, int gi, Smem<R>& sh, int& phase,
-                            const cplx<R>* q, const ColRef& c, int k, int j) {
-  const int N = P.N, n = P.n, Pm = P.P_mgs;
-  cplx<R> acc = c_zero<R>();
+template <class R, bool S>
+__device__ __forceinline__ void mgs_project(const DevPlan& P, const Group& g, int gi, Smem<R>& sh, int& phase, const cplx<R>* q,
+                            const OwnedCol& c, int k, int j) {
+  assume_shared<S>(c);
+  const int N = P.N, n = P.n, Pm = P.P_mgs, TT = 32 * g.gw;
+  cplx<R> v[kMaxElems];
 #pragma unroll
   for (int r = 0; r < kMaxElems; ++r) {
-    const int i = g.p + r * Pm;
-    if (i < N) {
-      const cplx<R> v = c_conj_mul(q[r], load_c<R>(c.p, c.S, i));
-      acc = (r == 0) ? v : c_add(acc, v);
-    }
+    const int i = g.p + r * TT;
+    v[r] = i < N ? c_conj_mul(q[r], load_c<R>(c.a.p, c.a.S, i)) : c_zero<R>();
   }
   cplx<R>* sm = sh.tree + gi * 32 * g.gw;
-  cplx<R> rkj = group_tree(acc, g, Pm, N, sm);
-  if (g.p == 0) store_c<R>(W.Rm, (long)n * (n + 1), (long)j * n + k, rkj);
+  cplx<R> rkj = mgs_reduce(v, g, Pm, N, sm);
+  if (g.p == 0) store_c<R>(c.r.p, c.r.S, k, rkj);
   rkj = group_bcast_c<R>(g, gi, rkj, sh, phase);
   if (j < n || k < n - 1) {
 #pragma unroll
     for (int r = 0; r < kMaxElems; ++r) {
-      const int i = g.p + r * Pm;
-      if (i < N) store_c<R>(c.p, c.S, i, c_sub(load_c<R>(c.p, c.S, i), c_mul(rkj, q[r])));
+      const int i = g.p + r * TT;
+      if (i < N) store_c<R>(c.a.p, c.a.S, i, c_sub(load_c<R>(c.a.p, c.a.S, i), c_mul(rkj, q[r])));
     }
   }
 }
 
 // Column-pipelined right-looking MGS.  Column j is owned
 // by group j mod G (group id = block + nblocks * group-in-CTA, so
-// consecutive columns sit on different SMs); the owner keeps its columns in
-// shared memory for the whole factorisation, normalises column k+1 as soon
-// as q_k has been applied (look-ahead), and publishes q_{k+1} with a release
-// flag.  Consumers read each q_k once from L2 into registers.
-template <class R, class Team>
-__device__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
-                    unsigned long long epoch, double sqrt_eps) {
+// consecutive columns sit on different SMs).  The owner keeps its columns,
+// their R entries and 1/r_jj in shared memory for the whole factorisation
+// (flushed to global at the end, so no release fence ever waits on them),
+// normalises column k+1 as soon as q_k has been applied (look-ahead) and
+// publishes q_{k+1} with a flag.  Consumers read q_k once (L2 for the grid
+// team, DSMEM for the cluster team, local smem for the block team).
+template <class R, class Team, bool S>
+__device__ __forceinline__ void mgs_run(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
+                                        double* pmax_sm, unsigned long long epoch, double sqrt_eps) {
   constexpr int L = limbs_of<R>::L;
+  if constexpr (S) {
+    if (!__isShared(colsm)) __builtin_unreachable();
+  }
   const int N = P.N, n = P.n, Pm = P.P_mgs;
-  const long SA = (long)N * (n + 1);
-  const int gm = Pm / 32;
+  const long SA = (long)N * (n + 1), SR = (long)n * (n + 1);
+  const int gm = P.mgs_gw;
+  const int TT = 32 * gm;
   const int gpc = kWarps / gm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gi = warp / gm;
@@ -664,15 +805,23 @@ __device__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& 
   const int G = nb * gpc;
   const int me = team.block + nb * gi;
   if (me > n) return;  // owns no column
-  auto own = [&](int j) -> ColRef {
-    return colsm ? ColRef{colsm + (long)(j / nb) * 2 * L * N, (long)N} : ColRef{W.A + (long)j * N, SA};
+  const int cols = (n + 1 + nb - 1) / nb;
+  double* rbase = colsm ? colsm + (size_t)cols * 2 * L * N : nullptr;
+  double* ibase = colsm ? rbase + (size_t)cols * 2 * L * (n + 1) : nullptr;
+  auto own = [&](int j) -> OwnedCol {
+    if (colsm) {
+      const int slot = j / nb;
+      return OwnedCol{ColRef{colsm + (long)slot * 2 * L * N, (long)N},
+                      ColRef{rbase + (long)slot * 2 * L * (n + 1), (long)(n + 1)}, ibase + (long)slot * L, 1, 0};
+    }
+    return OwnedCol{ColRef{W.A + (long)j * N, SA}, ColRef{W.Rm + (long)j * n, SR}, W.inv, (long)n, j};
   };
   if (colsm) {  // stage the owned columns (each thread its own rows: no sync needed)
     for (int j = me; j <= n; j += G) {
-      const ColRef c = own(j);
+      const ColRef c = own(j).a;
 #pragma unroll
       for (int r = 0; r < kMaxElems; ++r) {
-        const int i = g.p + r * Pm;
+        const int i = g.p + r * TT;
         if (i < N) store_c<R>(c.p, c.S, i, ldcg_c<R>(W.A + (long)j * N, SA, i));
       }
     }
@@ -683,7 +832,10 @@ __device__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& 
   // q_k travels through global memory (grid team, or no shared staging),
   // else it is read from the owner CTA's shared memory (local or DSMEM)
   const bool q_global = Team::kQInGlobal || colsm == nullptr;
-  if (me == 0) alive = mgs_normalize<R, Team>(P, W, team, g, gi, sh, phase, own(0), q_global, 0, epoch, sqrt_eps);
+  const bool pmax_shared = !Team::kQInGlobal && pmax_sm != nullptr;
+  double* pmx = pmax_shared ? pmax_sm : nullptr;
+  if (me == 0)
+    alive = mgs_normalize<R, Team, S>(P, W, team, g, gi, sh, phase, own(0), q_global, pmx, 0, 0.0, epoch, sqrt_eps);
   for (int k = 0; k < n && alive && k < last_owned; ++k) {
     const bool mine = (k % G == me);
     if (!mine) {
@@ -693,44 +845,92 @@ __device__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& 
       phase ^= 1;
       if (st != 0) return;  // rank failure of column k, or abort
     }
+    const bool next_mine = ((k + 1) % G == me) && k + 1 < n;
+    unsigned long long* dbg = (W.prof && next_mine && g.p == 0) ? W.prof + kProfSlots + 6 * (k + 1) : nullptr;
+    if (dbg) {
+      dbg[0] = gtimer();
+      dbg[1] = clock64();
+    }
     cplx<R> q[kMaxElems];
+    double prev = 0.0;
     {
       const double* qp;
+      const double* pm;
       long qS;
       if (mine) {
-        const ColRef ck = own(k);
+        const ColRef ck = own(k).a;
         qp = ck.p;
         qS = ck.S;
+        pm = pmx ? pmx + k : W.rmaxp + k;
       } else if (q_global) {
         qp = W.A + (long)k * N;
         qS = SA;
+        pm = pmx ? nullptr : W.rmaxp + k;
       } else {
         const double* loc = colsm + (long)(k / nb) * 2 * L * N;
-        qp = nb == 1 ? loc : cooperative_groups::this_cluster().map_shared_rank(const_cast<double*>(loc), k % nb);
+        qp = loc;  // nb == 1: local shared memory; else read below through DSMEM
         qS = N;
+        pm = nb == 1 ? pmx + k : cooperative_groups::this_cluster().map_shared_rank(pmx + k, k % nb);
       }
+      const bool remote = !mine && !q_global && nb > 1;
+      if (next_mine && g.p == 0) {
+        if (pmx && !mine && q_global)  // cluster/block team without shared staging
+          pm = nb == 1 ? pmx + k : cooperative_groups::this_cluster().map_shared_rank(pmx + k, k % nb);
+        prev = (pmx || mine) ? *(volatile const double*)pm : __ldcg(pm);
+      }
+      const uint32_t qremote = remote ? mapa_u32(smem_u32(qp), (uint32_t)(k % nb)) : 0u;
 #pragma unroll
       for (int r = 0; r < kMaxElems; ++r) {
-        const int i = g.p + r * Pm;
-        if (i < N) q[r] = (!mine && q_global) ? ldcg_c<R>(qp, qS, i) : load_c<R>(qp, qS, i);
+        const int i = g.p + r * TT;
+        if (i < N) {
+          if (remote)
+            q[r] = ldsc_c<R>(qremote, qS, i);
+          else
+            q[r] = (!mine && q_global && Team::kGrid) ? ldcg_c<R>(qp, qS, i) : load_c<R>(qp, qS, i);
+        }
       }
+      if (dbg) dbg[2] = clock64() + (unsigned long long)(r_hi(q[0].re) == 12345.0);  // after the loads land
     }
     int j = k + 1 + ((me - (k + 1)) % G + G) % G;  // first owned column > k
     for (; j <= n; j += G) {
-      const ColRef c = own(j);
-      mgs_project<R>(P, W, g, gi, sh, phase, q, c, k, j);
+      const OwnedCol c = own(j);
+      mgs_project<R, S>(P, g, gi, sh, phase, q, c, k, j);
       if (j == k + 1 && j < n) {
-        if (!mgs_normalize<R, Team>(P, W, team, g, gi, sh, phase, c, q_global, j, epoch, sqrt_eps)) alive = false;
+        if (dbg) dbg[3] = clock64();
+        if (!mgs_normalize<R, Team, S>(P, W, team, g, gi, sh, phase, c, q_global, pmx, j, prev, epoch, sqrt_eps))
+          alive = false;
+        if (dbg) {
+          dbg[4] = clock64();
+          dbg[5] = gtimer();
+        }
       }
     }
   }
+  if (colsm && alive) {  // flush R columns and inverses of the owned columns
+    for (int j = me; j <= n; j += G) {
+      const OwnedCol c = own(j);
+      const int rows = j < n ? j + 1 : n;
+      for (int k = g.p; k < rows; k += 32 * g.gw)
+        store_c<R>(W.Rm + (long)j * n, SR, k, load_c<R>(c.r.p, c.r.S, k));
+      if (j < n && g.p == 0) store_r<R>(W.inv, n, j, load_r<R>(c.inv, 1, 0));
+    }
+  }
+}
+
+template <class R, class Team>
+__device__ __noinline__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
+                                 double* pmax_sm, unsigned long long epoch, double sqrt_eps) {
+  if (colsm)
+    mgs_run<R, Team, true>(P, W, team, sh, colsm, pmax_sm, epoch, sqrt_eps);
+  else
+    mgs_run<R, Team, false>(P, W, team, sh, colsm, pmax_sm, epoch, sqrt_eps);
 }
 
 // Back substitution R dx = y, dx_k = (y_k - sum_{j>k} r_kj dx_j) * (1/r_kk),
 // column-oriented in one CTA with the next column of R prefetched one step
 // ahead (L2 latency off the dependency chain); then u = max|dx|, x += dx.
 template <class R>
-__device__ double backsub_update(const DevPlan& P, const Work& W, Smem<R>& sh) {
+__device__ __noinline__ double backsub_update(const DevPlan& P, const Work& W, Smem<R>& sh) {
   const int n = P.n;
   const long SR = (long)n * (n + 1);
   cplx<R> acc[kMaxRowsPerThread], cur[kMaxRowsPerThread], nxt[kMaxRowsPerThread];
@@ -791,7 +991,7 @@ struct History {
 };
 
 template <class R>
-__device__ void predict(const DevPlan& P, const Work& W, const History& H, double tau) {
+__device__ __noinline__ void predict(const DevPlan& P, const Work& W, const History& H, double tau) {
   const int n = P.n, d = H.count - 1;
   const long HS = 2L * limbs_of<R>::L * n;
   for (int i = threadIdx.x; i < n; i += kThreads) {
@@ -811,7 +1011,7 @@ __device__ void predict(const DevPlan& P, const Work& W, const History& H, doubl
 }
 
 template <class R>
-__device__ void push_history(const DevPlan& P, const Work& W, History& H, double t) {
+__device__ __noinline__ void push_history(const DevPlan& P, const Work& W, History& H, double t) {
   const int n = P.n;
   const long HS = 2L * limbs_of<R>::L * n;
   double* dst = W.hist + (long)H.next * HS;
@@ -877,7 +1077,7 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
     }
     ++epoch;
     pc.lap(W.prof + PROF_SLOTS);
-    mgs<R, Team>(P, W, team, sh, colsm, epoch, sqrt_eps);
+    mgs<R, Team>(P, W, team, sh, colsm, Team::kQInGlobal ? nullptr : sh.pmax, epoch, sqrt_eps);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     pc.lap(W.prof + PROF_MGS);
     if (ld_acquire(W.ctl + CTL_RANK) == epoch) {

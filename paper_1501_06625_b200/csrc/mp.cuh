@@ -260,7 +260,7 @@ PT_HD dd r_mul_d(dd a, double b) {  // multiprec.hpp:134-139
   e = add64(e, mul64(a.lo, b));
   return dd_norm(p, e);
 }
-PT_HDI dd r_div(dd a, dd b) {  // multiprec.hpp:145-155
+PT_HD dd r_div(dd a, dd b) {  // multiprec.hpp:145-155
   double q1 = div64(a.hi, b.hi);
   if (!finite(q1)) return {q1, 0.0};
   dd r = r_sub(a, r_mul_d(b, q1));
@@ -274,7 +274,7 @@ PT_HDI dd r_div(dd a, dd b) {  // multiprec.hpp:145-155
 // Negative argument: the reference throws std::domain_error
 // (multiprec.hpp:178); the device returns NaN instead (never reached on the
 // tracker path, whose sqrt arguments are sums of squares).
-PT_HDI dd r_sqrt(dd a) {  // multiprec.hpp:176-189
+PT_HD dd r_sqrt(dd a) {  // multiprec.hpp:176-189
   if (a.hi == 0.0 && a.lo == 0.0) return {0.0, 0.0};
   if (a.hi < 0.0) return {bitsd(0x7ff8000000000000ull), 0.0};
   double x = div64(1.0, sqrt64(a.hi));

@@ -38,14 +38,26 @@ inline int pow2ceil(int x) {
 // Canonical widths; the oracle uses the same rules.
 inline int width_eval(int K) { return std::min(256, std::max(32, pow2ceil((K + 15) / 16))); }
 inline int width_mgs(int N) { return std::min(256, std::max(32, pow2ceil((N + 1) / 2))); }
+// warps per MGS group: enough for one element per thread up to N = 256 (the
+// canonical width only fixes the partials, not who computes the products)
+inline int mgs_group_warps(int N) {
+  const int P = width_mgs(N);
+  if (N > 256) return 8;
+  return std::max(P / 32, std::min(8, pow2ceil((N + 31) / 32)));
+}
 
 struct SlotTask {
   int32_t row, col;
   int32_t g_beg, g_cnt;
   int32_t f_beg, f_cnt;  // f_cnt == -1: shared with g
-  int32_t gw;            // group width in warps = max canonical width / 32
+  int32_t gw;            // group width in warps = max canonical width / 32; 0 = lane task
   int32_t pad;
 };
+
+// Tasks whose sums have at most kLaneK(L) contributions on each side run one
+// per lane (the width-32 canonical tree then only has its off = 4, 2, 1
+// levels, evaluated sequentially by that lane: same shape, same bits).
+inline int lane_k(int L) { return L == 4 ? 4 : 8; }
 
 struct HostPlan {
   int n = 0, N = 0, L = 1;
@@ -54,7 +66,7 @@ struct HostPlan {
   int64_t ws_len = 0;  // complex entries in the monomial workspace
   // slots
   std::vector<SlotTask> tasks;
-  int32_t class_beg[5] = {0, 0, 0, 0, 0};  // tasks with gw = 8,4,2,1
+  int32_t class_beg[6] = {0, 0, 0, 0, 0, 0};  // lane tasks, then gw = 8,4,2,1
   std::vector<int32_t> ctr_coef, ctr_ws;
   // coefficients of all terms of g then f, complex SoA [2][L][n_coef]
   std::vector<double> coef;
@@ -246,17 +258,18 @@ inline HostPlan compile(const pt_system_desc* g, const pt_system_desc* f, int L)
       }
       check(P.ctr_coef.size() < ((size_t)1 << 31), "too many contributions");
       tk.gw = w / 32;
+      if (tk.g_cnt <= lane_k(L) && (tk.f_cnt < 0 || tk.f_cnt <= lane_k(L))) tk.gw = 0;
       tasks.push_back(tk);
     }
   }
-  // group tasks by width class (8, 4, 2, 1 warps); stable within a class
-  const int classes[4] = {8, 4, 2, 1};
-  for (int c = 0; c < 4; ++c) {
+  // group tasks by class (lane tasks, then 8, 4, 2, 1 warps); stable within a class
+  const int classes[5] = {0, 8, 4, 2, 1};
+  for (int c = 0; c < 5; ++c) {
     P.class_beg[c] = (int32_t)P.tasks.size();
     for (auto& tk : tasks)
       if (tk.gw == classes[c]) P.tasks.push_back(tk);
   }
-  P.class_beg[4] = (int32_t)P.tasks.size();
+  P.class_beg[5] = (int32_t)P.tasks.size();
   if (P.ctr_coef.empty()) {
     P.ctr_coef.push_back(0);
     P.ctr_ws.push_back(-1);

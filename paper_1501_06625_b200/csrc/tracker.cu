@@ -72,7 +72,7 @@ Layout make_layout(int L, int n, int N, long ws_len) {
   o.ctl = u;
   u += 32;
   o.prof = u;
-  u += 32;
+  u += kProfSlots + 6 * (n + 2) + 32;
   o.uslice = u;
   return o;
 }
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lstsq(DevPlan P, Work W, unsign
   __shared__ Smem<R> sh;
   extern __shared__ double dyn_smem[];
   const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
-  mgs<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, epoch, kSqrtEps<R>());
+  mgs<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, nullptr, epoch, kSqrtEps<R>());
   if (!team.sync(&sh.flag)) {
     if (team.block == 0 && threadIdx.x == 0) *status = PT_E_TIMEOUT;
     return;
@@ -316,6 +316,48 @@ __global__ void k_latency(double* out, double seed) {
   out[14] = h;
 }
 
+// MGS building blocks on one warp (group width 1, N = 64), in cycles:
+// out[0] group_tree<cplx<dd>>, [1] mgs_project, [2] c_conj_mul, [3] dd sqrt, [4] dd div
+__global__ void k_mgs_pieces(double* out) {
+  __shared__ Smem<dd> sh;
+  __shared__ double col[4 * 64], rcol[4 * 65], invb[2];
+  const int lane = threadIdx.x;
+  const Group g{1, lane, 1};
+  for (int i = lane; i < 4 * 64; i += 32) col[i] = 1.0 + 1e-3 * i;
+  __syncwarp();
+  cplx<dd> q[kMaxElems];
+  for (int r = 0; r < 2; ++r) q[r] = cplx<dd>{{0.5 + 1e-4 * lane, 1e-20}, {0.25, 0}};
+  DevPlan P{};
+  P.n = 64;
+  P.N = 64;
+  P.P_mgs = 32;
+  P.mgs_gw = 1;
+  OwnedCol c{ColRef{col, 64}, ColRef{rcol, 65}, invb, 1, 0};
+  int phase = 0;
+  cplx<dd> acc{{1.0 + lane, 0}, {0.5, 0}};
+  long long t0 = clock64();
+  cplx<dd> t = group_tree(acc, g, 32, 64, sh.tree);
+  __syncwarp();
+  long long t1 = clock64();
+  mgs_project<dd, true>(P, g, 0, sh, phase, q, c, 3, 10);
+  __syncwarp();
+  long long t2 = clock64();
+  cplx<dd> z = c_conj_mul(q[0], q[1]);
+  long long t3 = clock64();
+  dd sq = r_sqrt(z.re);
+  long long t4 = clock64();
+  dd dv = r_div(dd{1.0, 0.0}, sq);
+  long long t5 = clock64();
+  if (lane == 0) {
+    out[0] = (double)(t1 - t0);
+    out[1] = (double)(t2 - t1);
+    out[2] = (double)(t3 - t2);
+    out[3] = (double)(t4 - t3);
+    out[4] = (double)(t5 - t4);
+    out[15] = t.re.hi + dv.hi + col[5];
+  }
+}
+
 // Grid barrier cost: every CTA crosses `iters` GridTeam barriers.
 __global__ void k_barrier(unsigned long long* ctl, int iters, double* out) {
   __shared__ int flag;
@@ -417,8 +459,8 @@ constexpr size_t kSmemBudget = 200 * 1024;  // dynamic smem ceiling per CTA (227
 
 // bytes of owned MGS columns per CTA, 0 when they do not fit (global fallback)
 size_t mgs_smem_bytes(int L, int N, int n, int nblocks) {
-  const size_t cols = (size_t)(n + 1 + nblocks - 1) / nblocks;
-  const size_t bytes = cols * 2 * L * (size_t)N * 8;
+  const int cols = (n + 1 + nblocks - 1) / nblocks;
+  const size_t bytes = mgs_stage_doubles(L, N, n, cols) * 8;
   return bytes <= kSmemBudget ? bytes : 0;
 }
 
@@ -434,8 +476,8 @@ int dispatch_grid_size(pt_plan* p, const void* fn) {
   if (rc) return rc;
   const int cap = std::max(1, per_sm) * sms;
   // enough CTAs that each phase has about one unit of work per warp / group
-  const long ntasks = p->dp.class_beg[4];
-  const int gpc_mgs = kWarps / (p->dp.P_mgs / 32);
+  const long ntasks = p->dp.class_beg[5];
+  const int gpc_mgs = kWarps / p->dp.mgs_gw;
   long want = 1;
   want = std::max(want, (long)(p->M + kThreads - 1) / kThreads);
   want = std::max(want, (ntasks + kWarps - 1) / kWarps);
@@ -637,6 +679,7 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     dp.N = hp.N;
     dp.M = p->M;
     dp.P_mgs = ptplan::width_mgs(hp.N);
+    dp.mgs_gw = ptplan::mgs_group_warps(hp.N);
     dp.mono_size = (const int32_t*)(base + offs[0]);
     dp.mono_vbeg = (const int32_t*)(base + offs[1]);
     dp.mono_out = (const int32_t*)(base + offs[2]);
@@ -645,7 +688,7 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     dp.mono_exp = (const int32_t*)(base + offs[5]);
     dp.ws_len = hp.ws_len;
     dp.tasks = (const ptplan::SlotTask*)(base + offs[6]);
-    for (int c = 0; c < 5; ++c) dp.class_beg[c] = hp.class_beg[c];
+    for (int c = 0; c < 6; ++c) dp.class_beg[c] = hp.class_beg[c];
     dp.ctr_coef = (const int32_t*)(base + offs[7]);
     dp.ctr_ws = (const int32_t*)(base + offs[8]);
     dp.coef = (const double*)(base + offs[9]);
@@ -801,6 +844,10 @@ int pt_microbench(int device, int32_t what, double* out) {
     PT_CUDA(cudaLaunchCooperativeKernel((const void*)&k_barrier, dim3(blocks), dim3(kThreads), args, 0, 0));
   } else if (what == 2) {
     k_pingpong<<<prop.multiProcessorCount, 32>>>(u, 10000, d);
+  } else if (what == 3) {
+    k_mgs_pieces<<<1, 32>>>(d);
+    PT_CUDA(cudaDeviceSynchronize());
+    k_mgs_pieces<<<1, 32>>>(d);
   } else {
     return fail(PT_E_INVAL, "unknown microbenchmark");
   }
@@ -809,6 +856,17 @@ int pt_microbench(int device, int32_t what, double* out) {
   PT_CUDA(cudaMemcpy(out, d, 16 * 8, cudaMemcpyDeviceToHost));
   cudaFree(d);
   cudaFree(u);
+  return PT_OK;
+}
+
+int pt_plan_mgs_timeline(pt_plan* p, double* out, int32_t count) {
+  if (!p || !out) return PT_E_INVAL;
+  PT_CUDA(cudaSetDevice(p->device));
+  PT_CUDA(cudaStreamSynchronize(p->stream));
+  const int m = std::min(count, 6 * (p->n + 1));
+  std::vector<unsigned long long> h(m);
+  PT_CUDA(cudaMemcpy(h.data(), carve(p->dwork, p->uwork, p->lay, 0).prof + kProfSlots, m * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < m; ++i) out[i] = (double)h[i];
   return PT_OK;
 }
 
@@ -1012,7 +1070,8 @@ int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, co
     dp.n = n;
     dp.N = N;
     dp.P_mgs = ptplan::width_mgs(N);
-    const int gpc = kWarps / (dp.P_mgs / 32);
+    dp.mgs_gw = ptplan::mgs_group_warps(N);
+    const int gpc = kWarps / dp.mgs_gw;
     int per_sm = 0, sms = 0;
     const void* fn = prec == PT_D ? (const void*)&k_lstsq<double> : prec == PT_DD ? (const void*)&k_lstsq<dd> : (const void*)&k_lstsq<qd>;
     rc = occupancy_blocks(fn, device, &per_sm, &sms);

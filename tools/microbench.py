@@ -19,4 +19,7 @@ nat.check(nat.lib.pt_microbench(0, 1, nat.dptr(b)))
 out["grid_barrier_ns"] = float(b[0])
 nat.check(nat.lib.pt_microbench(0, 2, nat.dptr(b)))
 out["flag_one_way_ns"] = float(b[0])
+nat.check(nat.lib.pt_microbench(0, 3, nat.dptr(b)))
+out["mgs_pieces_cycles"] = dict(zip(["tree_cplx_dd", "project_dd_N64", "conj_mul_dd", "sqrt_dd", "div_dd"],
+                                    b[:5].tolist()))
 print(json.dumps(out))
