@@ -6,7 +6,7 @@ HOSTCXX  := $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo g++)
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 # --fmad=false + explicit _rn intrinsics: no FMA contraction anywhere (bit parity)
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -ccbin $(HOSTCXX) \
-            -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills $(EXTRA_NVFLAGS)
+            -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills --split-compile=0 $(EXTRA_NVFLAGS)
 PKG      := paper_1501_06625_b200
 SRC      := $(PKG)/csrc
 LIB      := $(PKG)/libpathtrack_b200.so

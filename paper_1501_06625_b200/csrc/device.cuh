@@ -60,6 +60,8 @@ struct DevPlan {
   const double* gamma;  // 2L limbs
   int relax_k;
   int mgs_smem;  // 1: MGS keeps owned columns in dynamic shared memory
+  int mgs_warp;  // 1: warp-per-column MGS + one-warp back substitution (mgs_warp.cuh, N <= 128)
+  int mgs_B;     // warp MGS: consecutive columns per CTA block (divides kWarps)
 };
 
 // One path's workspace.  All arrays are complex SoA unless noted.
@@ -270,8 +272,8 @@ struct ClusterTeam {
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
         return (int)(v & 1u);
       }
-      __nanosleep(32);
-      if ((++spins & 1023u) == 0 && (double)(gtimer() - t0) > kTimeoutNs) {
+      if (++spins > 512u) __nanosleep(20);
+      if ((spins & 1023u) == 0 && (double)(gtimer() - t0) > kTimeoutNs) {
         atomicExch(ctl + CTL_ABORT, 1ull);
         __trap();  // hardware cluster barriers cannot be abandoned: kill the launch instead of hanging
       }
@@ -407,6 +409,7 @@ struct Smem {
   double red[kWarps];
   double pmax[kMaxCols];    // MGS prefix max of r_kk (cluster / block teams)
   int flag;
+  int mgs_seq;              // MGS sweeps completed by this CTA in this launch (mbarrier phase parity)
 };
 
 // ---------------------------------------------------------------------------
@@ -981,6 +984,12 @@ __device__ __noinline__ double backsub_update(const DevPlan& P, const Work& W, S
   return block_nan_max(u, sh.red);
 }
 
+}  // namespace ptdev
+
+#include "mgs_warp.cuh"
+
+namespace ptdev {
+
 // ---------------------------------------------------------------------------
 // (3) predictor -- one CTA
 // ---------------------------------------------------------------------------
@@ -1077,14 +1086,23 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
     }
     ++epoch;
     pc.lap(W.prof + PROF_SLOTS);
-    mgs<R, Team>(P, W, team, sh, colsm, Team::kQInGlobal ? nullptr : sh.pmax, epoch, sqrt_eps);
+    if (P.mgs_warp)
+      mgs_warp<R, Team>(P, W, team, sh, colsm, epoch, sqrt_eps);
+    else
+      mgs<R, Team>(P, W, team, sh, colsm, Team::kQInGlobal ? nullptr : sh.pmax, epoch, sqrt_eps);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     pc.lap(W.prof + PROF_MGS);
+    if (threadIdx.x == 0) ++sh.mgs_seq;  // read again only after the next team barrier
     if (ld_acquire(W.ctl + CTL_RANK) == epoch) {
       o.kind = NW_LINEAR_SOLVE;
       return o;
     }
-    if (team.block == 0) {
+    if (P.mgs_warp) {
+      if (team.block == 0 && threadIdx.x < 32) {
+        const double u = backsub_warp<R>(P, W);
+        if (threadIdx.x == 0) W.scal[0] = u;
+      }
+    } else if (team.block == 0) {
       const double u = backsub_update<R>(P, W, sh);
       if (threadIdx.x == 0) W.scal[0] = u;
     }

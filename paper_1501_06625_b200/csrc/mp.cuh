@@ -30,7 +30,11 @@
 #define PT_HDI __host__ __device__ inline
 // QD operations are hundreds of instructions each: compile them once and call
 // them, instead of inlining a 23-way sort at every use site.
+#if defined(PT_QD_INLINE) && PT_QD_INLINE
+#define PT_QDOP __host__ __device__ __forceinline__
+#else
 #define PT_QDOP __host__ __device__ __noinline__
+#endif
 #else
 #define PT_HD inline
 #define PT_HDI inline
@@ -370,6 +374,20 @@ PT_HD qd qd_distill(double (&m)[K]) {
 #pragma unroll
     for (int j = i; j >= 1; --j) m[j] = (j > pos) ? m[j - 1] : (j == pos ? v : m[j]);
     if (pos == 0) m[0] = v;
+  }
+#elif PT_QD_SORT == 3
+  // odd-even transposition sort: K rounds of adjacent compare-exchanges that
+  // swap only on strict |m[i]| < |m[i+1]| (stable), so the permutation equals
+  // the reference's stable insertion sort; constant depth K, no branches.
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+#pragma unroll
+    for (int i = r & 1; i + 1 < K; i += 2) {
+      const double a = m[i], b = m[i + 1];
+      const bool sw = mag(a) < mag(b);
+      m[i] = sw ? b : a;
+      m[i + 1] = sw ? a : b;
+    }
   }
 #else
 #pragma unroll

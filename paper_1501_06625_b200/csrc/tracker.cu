@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -102,12 +103,31 @@ __host__ __device__ inline Work carve(double* dbase, unsigned long long* ubase, 
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
+// Per-launch CTA prologue: MGS sweep counter and, for the mbarrier exchange
+// of the warp MGS, one receive barrier per column (phase = sweep parity).
+// The caller's team barrier publishes the initialisation.
+template <class R>
+__device__ void cta_prologue(const DevPlan& P, Smem<R>& sh, double* dyn_smem, int nblocks) {
+  if (threadIdx.x == 0) {
+    sh.mgs_seq = 0;
+    if (P.mgs_warp == 2) {
+      constexpr int L = limbs_of<R>::L;
+      uint64_t* bars = reinterpret_cast<uint64_t*>(dyn_smem + mgs_warp_slots_doubles(L, P.N, P.n, nblocks) +
+                                                   (long)P.n * mgs_warp_qs(L, P.N));
+      for (int k = 0; k < P.n; ++k) mbar_init(bars + k, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+}
+
 template <class R>
 __global__ void __launch_bounds__(kThreads, 1)
     k_track_grid(DevPlan P, Work W, pt_step_params sp, TrackIO io, unsigned long long epoch_base) {
   __shared__ Smem<R> sh;
   extern __shared__ double dyn_smem[];
   const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
+  cta_prologue<R>(P, sh, dyn_smem, (int)gridDim.x);
+  __syncthreads();
   track_path<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
 }
 
@@ -121,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ double dyn_smem[];
   for (int i = threadIdx.x; i < kMaxCols; i += kThreads) s_flags[i] = 0;
   const ClusterTeam team{W.ctl, (int)cluster_nranks(), (int)cluster_rank(), s_flags};
+  cta_prologue<R>(P, sh, dyn_smem, team.nblocks);
   team.sync(&sh.flag);
   track_path<R, ClusterTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
   team.sync(&sh.flag);  // keep every CTA's shared memory alive until all DSMEM reads are done
@@ -138,6 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int i = threadIdx.x; i < kMaxCols; i += kThreads) s_flags[i] = 0;
   const Work W = carve(dbase, ubase, lay, blockIdx.x);
   const BlockTeam team{W.ctl, 1, 0, s_flags};
+  cta_prologue<R>(P, sh, dyn_smem, 1);
+  __syncthreads();
   const long PS = 2L * limbs_of<R>::L * P.n;
   for (;;) {
     if (threadIdx.x == 0) s_path = (int)atomicAdd(queue, 1ull);
@@ -183,6 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lstsq(DevPlan P, Work W, unsign
   __shared__ Smem<R> sh;
   extern __shared__ double dyn_smem[];
   const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
+  cta_prologue<R>(P, sh, dyn_smem, (int)gridDim.x);
+  __syncthreads();
   mgs<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, nullptr, epoch, kSqrtEps<R>());
   if (!team.sync(&sh.flag)) {
     if (team.block == 0 && threadIdx.x == 0) *status = PT_E_TIMEOUT;
@@ -405,6 +430,7 @@ struct pt_plan {
   unsigned long long* uwork = nullptr;
   int grid_blocks = 1;
   size_t grid_dyn_smem = 0;   // dynamic smem of k_track_grid / k_eval
+  int grid_warp = 0, cluster_warp = 0, batch_warp = 0;  // warp-per-column MGS per engine
   int engine = 0;             // 0 grid, 1 cluster (single path)
   int cluster_size = 0;       // CTAs of the cluster engine (0: unavailable)
   size_t cluster_dyn_smem = 0;
@@ -464,6 +490,31 @@ size_t mgs_smem_bytes(int L, int N, int n, int nblocks) {
   return bytes <= kSmemBudget ? bytes : 0;
 }
 
+// MGS variant of an engine with `nblocks` CTAs (DevPlan::mgs_warp) and its
+// dynamic shared memory:
+//   2  warp-per-column MGS, q_k pushed by st.async into every consuming CTA
+//      (cluster / block teams; needs the whole Q buffer in shared memory);
+//   1  warp-per-column MGS, q_k through shared memory / DSMEM / L2 + flags;
+//   0  group MGS of device.cuh (any N up to 1024).
+// QD keeps the group MGS: its column chain is issue bound, and groups of
+// 2+ warps put one element per thread on it.  PT_MGS_WARP=<0|1|2> caps it.
+size_t engine_smem(int L, int N, int n, int nblocks, bool cluster_or_block, int* warp) {
+  const char* e = getenv("PT_MGS_WARP");
+  int cap = e ? atoi(e) : (L == 4 ? 0 : 2);
+  if (!cluster_or_block) cap = std::min(cap, 1);
+  *warp = 0;
+  if (N <= kWarpMgsMaxN) {
+    if (cap >= 2 && mgs_warp_bytes(L, N, n, nblocks, true) <= kSmemBudget) *warp = 2;
+    else if (cap >= 1 && mgs_warp_bytes(L, N, n, nblocks, false) <= kSmemBudget) *warp = 1;
+  }
+  return *warp ? mgs_warp_bytes(L, N, n, nblocks, *warp == 2) : mgs_smem_bytes(L, N, n, nblocks);
+}
+int warp_mgs_block() {
+  const char* e = getenv("PT_MGS_B");
+  const int b = e ? atoi(e) : 4;
+  return (b == 1 || b == 2 || b == 4 || b == 8) ? b : 4;
+}
+
 int set_dyn_smem(const void* fn, size_t bytes) {
   PT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(bytes, 1)));
   return PT_OK;
@@ -483,7 +534,7 @@ int dispatch_grid_size(pt_plan* p, const void* fn) {
   want = std::max(want, (ntasks + kWarps - 1) / kWarps);
   want = std::max(want, (long)(p->n + 1 + gpc_mgs - 1) / gpc_mgs);
   p->grid_blocks = (int)std::min<long>(want, std::min(cap, sms));
-  p->grid_dyn_smem = mgs_smem_bytes(p->L, p->N, p->n, p->grid_blocks);
+  p->grid_dyn_smem = engine_smem(p->L, p->N, p->n, p->grid_blocks, false, &p->grid_warp);
   for (const void* f : {fn, (const void*)&k_eval<R>}) {
     rc = set_dyn_smem(f, p->grid_dyn_smem);
     if (rc) return rc;
@@ -502,7 +553,8 @@ int setup_cluster(pt_plan* p) {
   PT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   p->cluster_size = 0;
   for (int c : {16, 8, 4, 2}) {
-    const size_t dyn = mgs_smem_bytes(p->L, p->N, p->n, c);
+    int warp = 0;
+    const size_t dyn = engine_smem(p->L, p->N, p->n, c, true, &warp);
     if (dyn == 0) continue;
     if (set_dyn_smem(fn, dyn)) return PT_E_CUDA;
     cudaLaunchConfig_t cfg = {};
@@ -520,6 +572,7 @@ int setup_cluster(pt_plan* p) {
     if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) == cudaSuccess && nclusters >= 1) {
       p->cluster_size = c;
       p->cluster_dyn_smem = dyn;
+      p->cluster_warp = warp;
       break;
     }
     cudaGetLastError();
@@ -558,6 +611,7 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
   if (p->engine == 1) {
     DevPlan dp = p->dp;
     dp.mgs_smem = p->cluster_dyn_smem > 0;
+    dp.mgs_warp = p->cluster_warp;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p->cluster_size);
     cfg.blockDim = dim3(kThreads);
@@ -575,6 +629,7 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
   }
   DevPlan dp = p->dp;
   dp.mgs_smem = p->grid_dyn_smem > 0;
+  dp.mgs_warp = p->grid_warp;
   pt_step_params spc = sp;
   TrackIO ioc = io;
   void* args[] = {&dp, &W, &spc, &ioc, &epoch};
@@ -680,6 +735,7 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     dp.M = p->M;
     dp.P_mgs = ptplan::width_mgs(hp.N);
     dp.mgs_gw = ptplan::mgs_group_warps(hp.N);
+    dp.mgs_B = warp_mgs_block();
     dp.mono_size = (const int32_t*)(base + offs[0]);
     dp.mono_vbeg = (const int32_t*)(base + offs[1]);
     dp.mono_out = (const int32_t*)(base + offs[2]);
@@ -933,7 +989,7 @@ static int ensure_batch(pt_plan* p) {
   const void* fn = p->prec == PT_D    ? (const void*)&k_track_batch<double>
                    : p->prec == PT_DD ? (const void*)&k_track_batch<dd>
                                       : (const void*)&k_track_batch<qd>;
-  p->batch_dyn_smem = mgs_smem_bytes(p->L, p->N, p->n, 1);
+  p->batch_dyn_smem = engine_smem(p->L, p->N, p->n, 1, true, &p->batch_warp);
   int rc = set_dyn_smem(fn, p->batch_dyn_smem);
   if (rc) return rc;
   cudaDeviceProp prop;
@@ -967,18 +1023,33 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   const int blocks = std::min(p->batch_blocks, n_paths);
   DevPlan bdp = p->dp;
   bdp.mgs_smem = p->batch_dyn_smem > 0;
+  bdp.mgs_warp = p->batch_warp;
+  // launched as clusters of one CTA: the warp MGS pushes q_k with st.async,
+  // which needs a cluster launch even when the cluster is the CTA itself
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = p->batch_dyn_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
   switch (p->prec) {
     case PT_D:
-      k_track_batch<double><<<blocks, kThreads, p->batch_dyn_smem, s>>>(bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
-                                                        n_paths, p->d_queue, epoch);
+      PT_CUDA(cudaLaunchKernelEx(&cfg, k_track_batch<double>, bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends,
+                                 d_stats, n_paths, p->d_queue, epoch));
       break;
     case PT_DD:
-      k_track_batch<dd><<<blocks, kThreads, p->batch_dyn_smem, s>>>(bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
-                                                    n_paths, p->d_queue, epoch);
+      PT_CUDA(cudaLaunchKernelEx(&cfg, k_track_batch<dd>, bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends,
+                                 d_stats, n_paths, p->d_queue, epoch));
       break;
     default:
-      k_track_batch<qd><<<blocks, kThreads, p->batch_dyn_smem, s>>>(bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends, d_stats,
-                                                    n_paths, p->d_queue, epoch);
+      PT_CUDA(cudaLaunchKernelEx(&cfg, k_track_batch<qd>, bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends,
+                                 d_stats, n_paths, p->d_queue, epoch));
       break;
   }
   PT_CUDA(cudaGetLastError());
@@ -1027,6 +1098,7 @@ int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J
   Work W = carve(p->dwork, p->uwork, p->lay, 0);
   DevPlan dp = p->dp;
   dp.mgs_smem = 0;
+  dp.mgs_warp = 0;
   void* args[] = {&dp, &W, &dx, &t, &dh, &dJ, &dr};
   const void* fn = p->prec == PT_D ? (const void*)&k_eval<double> : p->prec == PT_DD ? (const void*)&k_eval<dd> : (const void*)&k_eval<qd>;
   PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, p->grid_dyn_smem, p->stream));
