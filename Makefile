@@ -10,7 +10,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -ccbin $(HOSTCXX) \
 PKG      := paper_1501_06625_b200
 SRC      := $(PKG)/csrc
 LIB      := $(PKG)/libpathtrack_b200.so
-HDRS     := $(SRC)/mp.cuh $(SRC)/device.cuh $(SRC)/plan.hpp $(SRC)/work.hpp include/pathtrack_b200.h
+HDRS     := $(SRC)/mp.cuh $(SRC)/device.cuh $(SRC)/mgs_warp.cuh $(SRC)/plan.hpp $(SRC)/work.hpp include/pathtrack_b200.h
 
 all: $(LIB) oracle
 

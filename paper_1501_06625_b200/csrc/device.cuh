@@ -62,6 +62,7 @@ struct DevPlan {
   int mgs_smem;  // 1: MGS keeps owned columns in dynamic shared memory
   int mgs_warp;  // 1: warp-per-column MGS + one-warp back substitution (mgs_warp.cuh, N <= 128)
   int mgs_B;     // warp MGS: consecutive columns per CTA block (divides kWarps)
+  int bs_smem;   // warp back substitution stages R in CTA 0's dynamic shared memory
 };
 
 // One path's workspace.  All arrays are complex SoA unless noted.
@@ -76,6 +77,7 @@ struct Work {
   double* hmod;   // [N] |h_i| in binary64
   double* scal;   // [8] 0: update norm u
   double* dx;     // [2L][n] last Newton update
+  double* qg;     // [n][2L*N + 2] warp-MGS messages staged for the TMA multicast
   unsigned long long* flags;  // [n+1] MGS column-ready flags (epoch values)
   unsigned long long* ctl;    // [CTL_WORDS] barrier / abort / rank-fail
   unsigned long long* prof;   // [kProfSlots] phase time accumulators (ns, block 0)
@@ -332,6 +334,20 @@ __device__ __forceinline__ cplx<R> add_v(const cplx<R>& a, const cplx<R>& b) {
   return c_add(a, b);
 }
 
+// branch-free select (keeps independent chains in one basic block)
+__device__ __forceinline__ double pick(bool c, double a, double b) { return c ? a : b; }
+__device__ __forceinline__ dd pick(bool c, dd a, dd b) { return {c ? a.hi : b.hi, c ? a.lo : b.lo}; }
+__device__ __forceinline__ qd pick(bool c, const qd& a, const qd& b) {
+  qd r;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) r.c[l] = c ? a.c[l] : b.c[l];
+  return r;
+}
+template <class R>
+__device__ __forceinline__ cplx<R> pick(bool c, const cplx<R>& a, const cplx<R>& b) {
+  return {pick(c, a.re, b.re), pick(c, a.im, b.im)};
+}
+
 // A "group" is gw consecutive warps of a CTA (gw in {1,2,4,8}) that owns one
 // canonical sum of width Pw <= 32*gw; thread p of the group holds partial p.
 struct Group {
@@ -367,7 +383,7 @@ __device__ __forceinline__ T group_tree(T acc, const Group& g, int Pw, int K, T*
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     T other = shfl_down_r(acc, off);
-    if (g.p < off && g.p + off < K) acc = add_v(acc, other);
+    acc = pick(g.p < off && g.p + off < K, add_v(acc, other), acc);
   }
   return acc;
 }
@@ -1098,8 +1114,8 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       return o;
     }
     if (P.mgs_warp) {
-      if (team.block == 0 && threadIdx.x < 32) {
-        const double u = backsub_warp<R>(P, W);
+      if (team.block == 0) {
+        const double u = backsub_warp<R>(P, W, P.bs_smem ? colsm : nullptr, sh);
         if (threadIdx.x == 0) W.scal[0] = u;
       }
     } else if (team.block == 0) {

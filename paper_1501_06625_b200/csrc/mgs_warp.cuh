@@ -65,17 +65,12 @@ __device__ __forceinline__ T warp_canon(const T (&v)[E], int lane, int N, int P)
   T acc = v[0];
   if (P == 32) {
 #pragma unroll
-    for (int r = 1; r < E; ++r)
-      if (lane + 32 * r < N) acc = add_v(acc, v[r]);
+    for (int r = 1; r < E; ++r) acc = pick(lane + 32 * r < N, add_v(acc, v[r]), acc);
   } else {  // P == 64 (65 <= N <= 128): partial l = c[l] + c[l+64], partial l+32 = c[l+32] + c[l+96]
-    if constexpr (E > 2) {
-      if (lane + 64 < N) acc = add_v(acc, v[2]);
-    }
+    if constexpr (E > 2) acc = pick(lane + 64 < N, add_v(acc, v[2]), acc);
     if constexpr (E > 1) {
       T a1 = v[1];
-      if constexpr (E > 3) {
-        if (lane + 96 < N) a1 = add_v(a1, v[3]);
-      }
+      if constexpr (E > 3) a1 = pick(lane + 96 < N, add_v(a1, v[3]), a1);
       acc = add_v(acc, a1);  // off = 32 level: l + 32 < 65 <= N always
     }
   }
@@ -83,7 +78,7 @@ __device__ __forceinline__ T warp_canon(const T (&v)[E], int lane, int N, int P)
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     const T o = shfl_down_r(acc, off);
-    if (lane < off && lane + off < N) acc = add_v(acc, o);
+    acc = pick(lane < off && lane + off < N, add_v(acc, o), acc);
   }
   return acc;
 }
@@ -118,18 +113,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, int parity, unsigned long
     }
   }
 }
-__device__ __forceinline__ void st_async(uint32_t raddr, double v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
-               "r"(rbar)
-               : "memory");
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// One TMA bulk copy global -> the same shared-memory offset of every CTA in
+// `mask`, each completing `bytes` on its own copy of the barrier.
+__device__ __forceinline__ void bulk_multicast(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
 }
 
 // Dynamic shared memory of the warp MGS, per CTA (doubles / u64 words):
 //   [column slots: S * kWarps * 2L*N][Q buffer: n * QS][n mbarriers]
-// Q buffer row k = the message of column k: q_k (2L planes of N) + pmax_k.
+// Q buffer row k = the message of column k: q_k (2L planes of N), pmax_k, pad.
 // The Q buffer exists only in the mbarrier exchange (cluster / block teams);
 // the grid team exchanges q_k through L2 with release/acquire flags.
-__host__ __device__ inline long mgs_warp_qs(int L, int N) { return 2L * L * N + 1; }
+__host__ __device__ inline long mgs_warp_qs(int L, int N) { return 2L * L * N + 2; }  // even: 16-byte rows
 __host__ __device__ inline size_t mgs_warp_slots_doubles(int L, int N, int n, int C) {
   const int G = C * kWarps;
   const int slots = (n + 1 + G - 1) / G;
@@ -155,16 +158,20 @@ struct WarpMgs {
   unsigned long long epoch;
   double sqrt_eps;
 
-  __device__ double* slot_ptr(int ls) const { return colsm + (long)ls * CS; }
-  __device__ double* qbuf() const { return colsm + mgs_warp_slots_doubles(L, N, n, team.nblocks); }
-  __device__ uint64_t* bars() const { return reinterpret_cast<uint64_t*>(qbuf() + (long)n * mgs_warp_qs(L, N)); }
+  double* qb;     // Q buffer (mbarrier exchange)
+  uint64_t* bb;   // receive barriers
 
+  __device__ double* slot_ptr(int ls) const { return colsm + (long)ls * CS; }
+  __device__ double* qbuf() const { return qb; }
+  __device__ uint64_t* bars() const { return bb; }
+
+  // rows >= N read as zero (their lanes compute ignored values, branch-free)
   template <int E>
   __device__ __forceinline__ void load_col(const double* p, long S, cplx<R> (&a)[E]) const {
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       const int i = lane + 32 * r;
-      if (i < N) a[r] = load_c<R>(p, S, i);
+      a[r] = i < N ? load_c<R>(p, S, i) : c_zero<R>();
     }
   }
   template <int E>
@@ -187,33 +194,27 @@ struct WarpMgs {
     return mx;
   }
 
-  // Push the message of column j (q_j in a, pmax in lane 0) into the Q buffer
-  // of every CTA that owns a column > j, the CTA of column j+1 first.
-  // need: bit d set iff CTA d owns a column > j (lane-parallel ballot).
+  // Hand q_j to its consumers (mbarrier exchange).  Warps of this CTA read
+  // q_j from the owner's column slot after a local arrive on bar[j]; every
+  // other CTA that owns a column > j receives the message (q_j, pmax_j) by
+  // one TMA multicast from its global staging row W.qg[j] -- the copy runs on
+  // the L2 -> SM path, so the producer SM's shared-memory port stays free
+  // for the critical next column.  lane_maxcol: lane d < C holds maxcol(d).
   template <int E>
-  __device__ void push(int j, const cplx<R> (&a)[E], double pmax, int lane_maxcol) const {
-    const unsigned need = __ballot_sync(0xffffffffu, lane < team.nblocks && lane_maxcol > j);
-    int c1, w1, l1;
-    cm.owner(j + 1 <= n ? j + 1 : j, c1, w1, l1);
+  __device__ void handoff(int j, const cplx<R> (&a)[E], double pmax, int lane_maxcol) const {
     const long QS = mgs_warp_qs(L, N);
-    const uint32_t qloc = smem_u32(qbuf() + (long)j * QS), bloc = smem_u32(bars() + j);
-    unsigned rest = need;
-    for (int it = 0; rest; ++it) {
-      const int d = (it == 0 && (rest >> c1) & 1u) ? c1 : __ffs(rest) - 1;
-      rest &= ~(1u << d);
-      const uint32_t rq = mapa_u32(qloc, (uint32_t)d), rb = mapa_u32(bloc, (uint32_t)d);
-#pragma unroll
-      for (int r = 0; r < E; ++r) {
-        const int i = lane + 32 * r;
-        if (i < N) {
-#pragma unroll
-          for (int l = 0; l < L; ++l) {
-            st_async(rq + 8u * (uint32_t)(l * N + i), r_limb(a[r].re, l), rb);
-            st_async(rq + 8u * (uint32_t)((L + l) * N + i), r_limb(a[r].im, l), rb);
-          }
-        }
-      }
-      if (lane == 0) st_async(rq + 8u * (uint32_t)(2 * L * N), pmax, rb);
+    const unsigned need = __ballot_sync(0xffffffffu, lane < team.nblocks && lane_maxcol > j);
+    const unsigned remote = need & ~(1u << team.block);
+    double* msg = W.qg + (long)j * QS;
+    if (remote) {
+      store_col(msg, N, a);
+      if (lane == 0) msg[2 * L * N] = pmax;
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> async-proxy (TMA) reads
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if ((need >> team.block) & 1u) mbar_arrive_local(bars() + j);
+      if (remote) bulk_multicast(qbuf() + (long)j * QS, msg, (uint32_t)(QS * 8), bars() + j, (uint16_t)remote);
     }
   }
 
@@ -223,10 +224,11 @@ struct WarpMgs {
   // receive barrier must complete its phase): the column is still scaled
   // and pushed, CTL_RANK records the failure and the Newton step fails.
   template <int E, bool MB>
-  __device__ bool normalize(int j, cplx<R> (&a)[E], double* col, double prev, int lane_maxcol) const {
+  __device__ bool normalize(int j, cplx<R> (&a)[E], double* col, double prev, int lane_maxcol,
+                            unsigned long long* dbg = nullptr) const {
     R v[E];
 #pragma unroll
-    for (int r = 0; r < E; ++r) v[r] = (lane + 32 * r < N) ? c_norm_sqr(a[r]) : rconst<R>(0.0);
+    for (int r = 0; r < E; ++r) v[r] = c_norm_sqr(a[r]);  // rows >= N never enter the sum
     const R nrm2 = warp_canon(v, lane, N, P.P_mgs);
     int ok = 0;
     R inv = rconst<R>(0.0);
@@ -236,12 +238,10 @@ struct WarpMgs {
       const double d = r_hi(rjj);
       mx = d > prev ? d : prev;
       ok = d > sqrt_eps * mx;
-      if constexpr (!MB) {
-        if constexpr (Team::kQInGlobal)
-          W.rmaxp[j] = mx;
-        else
-          sh.pmax[j] = mx;
-      }
+      if constexpr (Team::kQInGlobal)
+        W.rmaxp[j] = mx;
+      else
+        sh.pmax[j] = mx;
       inv = r_div(rconst<R>(1.0), rjj);
       if (ok) {
         store_r<R>(W.inv, n, j, inv);
@@ -258,8 +258,9 @@ struct WarpMgs {
       store_col(col, N, a);
       if constexpr (Team::kQInGlobal) store_col(W.A + (long)j * N, SA, a);
     }
+    if (dbg) dbg[4] = clock64() + (unsigned long long)(r_hi(a[0].re) == 12345.0);
     if constexpr (MB) {
-      push(j, a, mx, lane_maxcol);
+      handoff(j, a, mx, lane_maxcol);
     } else {
       __syncwarp();
       if (lane == 0) team.publish(W.flags, j, epoch, !ok);
@@ -273,29 +274,33 @@ struct WarpMgs {
     load_col(col, N, a);
     cplx<R> v[E];
 #pragma unroll
-    for (int r = 0; r < E; ++r) v[r] = (lane + 32 * r < N) ? c_conj_mul(q[r], a[r]) : c_zero<R>();
+    for (int r = 0; r < E; ++r) v[r] = c_conj_mul(q[r], a[r]);  // rows >= N never enter the sum
     cplx<R> rkj = warp_canon(v, lane, N, P.P_mgs);
     if (lane == 0) store_c<R>(W.Rm, SR, (long)j * n + k, rkj);
     rkj = shfl0(rkj, 0);
     if (j < n || k < n - 1) {
 #pragma unroll
-      for (int r = 0; r < E; ++r)
-        if (lane + 32 * r < N) a[r] = c_sub(a[r], c_mul(rkj, q[r]));
+      for (int r = 0; r < E; ++r) a[r] = c_sub(a[r], c_mul(rkj, q[r]));  // rows >= N: ignored garbage
       store_col(col, N, a);
     }
   }
 
   template <int E, bool MB>
   __device__ void run() const {
+    if (!__isShared(colsm)) __builtin_unreachable();  // LDS/STS, not generic accesses
     const int c = team.block, G = cm.G();
     const int base = cm.base(c, w);
     const int par = sh.mgs_seq & 1;
     const int lane_maxcol = (MB && lane < team.nblocks) ? maxcol(lane) : -1;
-    if constexpr (MB) {  // arm this CTA's receive barriers for the columns it consumes
-      if (threadIdx.x == 0) {
+    if constexpr (MB) {  // arm the receive barriers of the columns this CTA consumes but does not own
+      if (w == kWarps - 1) {
         const int mc = maxcol(c);
         const uint32_t bytes = (uint32_t)(mgs_warp_qs(L, N) * 8);
-        for (int k = 0; k < n && k < mc; ++k) mbar_expect(bars() + k, bytes);
+        for (int k = lane; k < n && k < mc; k += 32) {
+          int oc, ow, ols;
+          cm.owner(k, oc, ow, ols);
+          if (oc != c) mbar_expect(bars() + k, bytes);
+        }
       }
     }
     if (base > n) return;  // owns no column
@@ -316,19 +321,52 @@ struct WarpMgs {
     }
     const int last = base + ((n - base) / G) * G;
     const long QS = mgs_warp_qs(L, N);
+    // owner of column k, tracked incrementally (no integer division on the chain):
+    // r0 = k mod G, rb = r0 mod B, kc = (r0 / B) mod C, bc = r0 / (B C), slot = k / G
+    int r0 = 0, rb = 0, kc = 0, bc = 0, kslot = 0;
+    int jn = base;  // smallest owned column > k
+    int mfirst = 0;
     for (int k = 0; k < n && k < last; ++k) {
-      int kc, kw, kls;
-      cm.owner(k, kc, kw, kls);
+      if (k > 0) {
+        if (++r0 == G) {
+          r0 = rb = kc = bc = 0;
+          ++kslot;
+        } else if (++rb == cm.B) {
+          rb = 0;
+          if (++kc == cm.C) {
+            kc = 0;
+            ++bc;
+          }
+        }
+      }
+      if (jn <= k) {
+        jn += G;
+        ++mfirst;
+      }
+      const int kw = bc * cm.B + rb, kls = kslot * kWarps + kw;
       const bool mine = kc == c && kw == w;
-      const bool next_mine = (k + 1) % G == base && k + 1 < n;
+      const bool next_mine = jn == k + 1 && k + 1 < n;
+      // timeline of the critical chain (tools/mgs_timeline.py): the owner of
+      // column k+1 records when it starts waiting for q_k, has it, has
+      // projected and normalised column k+1, and has pushed q_{k+1}
+      unsigned long long* dbg = (next_mine && lane == 0) ? W.prof + kProfSlots + 6 * (k + 1) : nullptr;
+      if (dbg) {
+        dbg[0] = gtimer();
+        dbg[1] = clock64();
+      }
       double prev = 0.0;
       if (mine) {
         load_col(slot_ptr(kls), N, q);
       } else if constexpr (MB) {
         mbar_wait(bars() + k, par, W.ctl);
-        const double* msg = qbuf() + (long)k * QS;
-        load_col(msg, N, q);
-        if (next_mine && lane == 0) prev = msg[2 * L * N];
+        if (kc == c) {  // the owner's slot in this CTA
+          load_col(slot_ptr(kls), N, q);
+          if (next_mine && lane == 0) prev = sh.pmax[k];
+        } else {
+          const double* msg = qbuf() + (long)k * QS;
+          load_col(msg, N, q);
+          if (next_mine && lane == 0) prev = msg[2 * L * N];
+        }
       } else {
         int st = 0;
         if (lane == 0) st = team.wait(W.flags, k, epoch);
@@ -342,7 +380,7 @@ struct WarpMgs {
 #pragma unroll
           for (int r = 0; r < E; ++r) {
             const int i = lane + 32 * r;
-            if (i < N) q[r] = ldcg_c<R>(W.A + (long)k * N, SA, i);
+            q[r] = i < N ? ldcg_c<R>(W.A + (long)k * N, SA, i) : c_zero<R>();
           }
           if (next_mine && lane == 0) prev = __ldcg(W.rmaxp + k);
         } else {
@@ -350,7 +388,7 @@ struct WarpMgs {
 #pragma unroll
           for (int r = 0; r < E; ++r) {
             const int i = lane + 32 * r;
-            if (i < N) q[r] = ldsc_c<R>(qa, N, i);
+            q[r] = i < N ? ldsc_c<R>(qa, N, i) : c_zero<R>();
           }
           if (next_mine && lane == 0) {
             double pv;
@@ -361,13 +399,17 @@ struct WarpMgs {
           }
         }
       }
+      if (dbg) dbg[2] = clock64() + (unsigned long long)(r_hi(q[0].re) == 12345.0);  // after the loads land
       // owned columns > k, smallest (the look-ahead column k+1) first
-      int m = k + 1 <= base ? 0 : (k + 1 - base + G - 1) / G;
-      for (int j = base + m * G; j <= n; j += G, ++m) {
+      int m = mfirst;
+      for (int j = jn; j <= n; j += G, ++m) {
         double* col = slot_ptr(m * kWarps + w);
         project(k, j, q, a, col);
-        if (j == k + 1 && j < n)
-          if (!normalize<E, MB>(j, a, col, prev, lane_maxcol) && !MB) return;
+        if (j == k + 1 && j < n) {
+          if (dbg) dbg[3] = clock64() + (unsigned long long)(r_hi(a[0].re) == 12345.0);
+          if (!normalize<E, MB>(j, a, col, prev, lane_maxcol, dbg) && !MB) return;
+          if (dbg) dbg[5] = gtimer();
+        }
       }
     }
   }
@@ -378,9 +420,12 @@ struct WarpMgs {
 template <class R, class Team, int E>
 __device__ __noinline__ void mgs_warp_e(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                                         unsigned long long epoch, double sqrt_eps) {
+  constexpr int L = limbs_of<R>::L;
+  double* qb = colsm + mgs_warp_slots_doubles(L, P.N, P.n, team.nblocks);
+  uint64_t* bb = reinterpret_cast<uint64_t*>(qb + (long)P.n * mgs_warp_qs(L, P.N));
   const WarpMgs<R, Team> m{P,    W, team, sh, colsm, ColMap{team.nblocks, P.mgs_B}, (int)(threadIdx.x & 31),
                            (int)(threadIdx.x >> 5), P.N, P.n, (long)P.N * (P.n + 1), (long)P.n * (P.n + 1),
-                           2L * limbs_of<R>::L * P.N, epoch, sqrt_eps};
+                           2L * L * P.N, epoch, sqrt_eps, qb, bb};
   if (P.mgs_warp == 2)
     m.template run<E, true>();
   else
@@ -398,66 +443,82 @@ __device__ __forceinline__ void mgs_warp(const DevPlan& P, const Work& W, const 
     mgs_warp_e<R, Team, 4>(P, W, team, sh, colsm, epoch, sqrt_eps);
 }
 
-// Back substitution R dx = y by one warp, rows lane + 32 r, column-oriented
-// with column j-1 of R prefetched while column j is applied; then
-// u = max|dx|, x += dx.  Returns u in every lane.
-template <class R, int E>
-__device__ __noinline__ double backsub_warp_e(const DevPlan& P, const Work& W) {
-  const int n = P.n, lane = threadIdx.x & 31;
+// Blocked back substitution R dx = y by the warps of one CTA (n <= 256):
+// warp b owns the rows 32b .. 32b+31 (one per lane).  For b = top block down
+// to 0: warp b solves its diagonal block sequentially (x_j = acc_j * (1/r_jj),
+// shuffle, acc_i -= r_ij x_j for its rows i < j -- a one-element chain per
+// step), publishes its x's in shared memory, and after one CTA barrier every
+// warp a < b applies them to its rows in descending j.  Every row therefore
+// subtracts r_ij x_j in exactly the oracle's order j = n-1 .. i+1.  Then
+// u = max|dx| and x += dx.  Returns u (valid in every thread of the CTA).
+template <class R>
+__device__ __noinline__ double backsub_blocked(const DevPlan& P, const Work& W, const double* Rs, const double* invs,
+                                               Smem<R>& sh, cplx<R>* xs) {
+  const int n = P.n, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long SR = (long)n * (n + 1);
-  cplx<R> acc[E], cur[E], nxt[E];
-  R inv[E];
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int i = lane + 32 * r;
-    if (i < n) {
-      acc[r] = load_c<R>(W.Rm, SR, (long)n * n + i);
-      inv[r] = load_r<R>(W.inv, n, i);
-      if (i < n - 1) cur[r] = load_c<R>(W.Rm, SR, (long)(n - 1) * n + i);
-    }
-  }
-  for (int j = n - 1; j >= 0; --j) {
-    const int ol = j & 31, orow = j >> 5;
-    cplx<R> xj = c_zero<R>();
-#pragma unroll
-    for (int r = 0; r < E; ++r)
-      if (r == orow && lane == ol) {
-        acc[r] = c_scale(acc[r], inv[r]);  // row j finished: dx_j
-        xj = acc[r];
+  const int nb = (n + 31) >> 5;
+  const int i = 32 * w + lane;
+  const bool row = w < nb && i < n;
+  cplx<R> acc = row ? load_c<R>(Rs, SR, (long)n * n + i) : c_zero<R>();
+  const R inv = row ? load_r<R>(invs, n, i) : rconst<R>(0.0);
+  for (int b = nb - 1; b >= 0; --b) {
+    const int j0 = 32 * b, jtop = min(n, j0 + 32) - 1;
+    if (w == b) {  // diagonal block: the sequential chain
+      const long long tb0 = clock64();
+      cplx<R> cur = (i < jtop) ? load_c<R>(Rs, SR, (long)jtop * n + i) : c_zero<R>();
+      for (int j = jtop; j >= j0; --j) {
+        const int jl = j - j0;
+        const cplx<R> nxt = (i < j - 1) ? load_c<R>(Rs, SR, (long)(j - 1) * n + i) : c_zero<R>();
+        const cplx<R> xs_l = c_scale(acc, inv);  // meaningful in lane jl: dx_j
+        acc = pick(lane == jl, xs_l, acc);
+        const cplx<R> xj = shfl0(xs_l, jl);
+        if (lane == jl) xs[j] = xj;
+        acc = pick(i < j, c_sub(acc, c_mul(cur, xj)), acc);
+        cur = nxt;
       }
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int i = lane + 32 * r;
-      if (i < j - 1) nxt[r] = load_c<R>(W.Rm, SR, (long)(j - 1) * n + i);
+      if (lane == 0 && W.prof) {  // debugging aid: cycles of the diagonal-block chains
+        W.prof[6] += (unsigned long long)(clock64() - tb0) + (unsigned long long)(r_hi(acc.re) == 12345.0);
+        W.prof[7] += (unsigned long long)(jtop - j0 + 1);
+      }
     }
-    xj = shfl0(xj, ol);
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int i = lane + 32 * r;
-      if (i < j) acc[r] = c_sub(acc[r], c_mul(cur[r], xj));
-      cur[r] = nxt[r];
+    __syncthreads();
+    if (w < b && row) {  // apply block b's x's, descending j
+      for (int j = jtop; j >= j0; --j) acc = c_sub(acc, c_mul(load_c<R>(Rs, SR, (long)j * n + i), xs[j]));
     }
   }
   double u = 0.0;
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int i = lane + 32 * r;
-    if (i < n) {
-      u = nan_max(u, c_mod_double(acc[r]));
-      store_c<R>(W.dx, n, i, acc[r]);
-      store_c<R>(W.x, n, i, c_add(load_c<R>(W.x, n, i), acc[r]));
-    }
+  if (row) {
+    u = c_mod_double(acc);
+    store_c<R>(W.dx, n, i, acc);
+    store_c<R>(W.x, n, i, c_add(load_c<R>(W.x, n, i), acc));
   }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) u = nan_max(u, __shfl_xor_sync(0xffffffffu, u, off));
-  return u;
+  return block_nan_max(u, sh.red);
 }
 
+// doubles of CTA 0's shared-memory copy of R (2L planes of n(n+1)) and 1/r_kk
+__host__ __device__ inline size_t backsub_stage_doubles(int L, int n) {
+  return (size_t)2 * L * n * (n + 1) + (size_t)L * n;
+}
+
+// Back substitution of the warp MGS, run by CTA 0 after the MGS barrier: all
+// its warps copy R (written by the column owners through L2) into shared
+// memory with independent coalesced loads, then run the blocked solve on
+// shared-memory reads.  stage == nullptr: R is read from global.
 template <class R>
-__device__ __forceinline__ double backsub_warp(const DevPlan& P, const Work& W) {
-  if (P.n <= 32) return backsub_warp_e<R, 1>(P, W);
-  if (P.n <= 64) return backsub_warp_e<R, 2>(P, W);
-  return backsub_warp_e<R, 4>(P, W);
+__device__ __noinline__ double backsub_warp(const DevPlan& P, const Work& W, double* stage, Smem<R>& sh) {
+  constexpr int L = limbs_of<R>::L;
+  const int n = P.n;
+  const double* Rs = W.Rm;
+  const double* invs = W.inv;
+  if (stage) {
+    const long nr = 2L * L * n * (n + 1), ni = (long)L * n;
+    for (long q = threadIdx.x; q < nr; q += blockDim.x) stage[q] = __ldcg(W.Rm + q);
+    for (long q = threadIdx.x; q < ni; q += blockDim.x) stage[nr + q] = __ldcg(W.inv + q);
+    __syncthreads();
+    Rs = stage;
+    invs = stage + nr;
+  }
+  return backsub_blocked<R>(P, W, Rs, invs, sh, sh.tree);  // sh.tree: kThreads complex >= n x's
 }
 
 }  // namespace ptdev

@@ -234,11 +234,14 @@ PT_HD double r_limb(double a, int) { return a; }
 PT_HD void r_set_limb(double& a, int, double v) { a = v; }
 
 // ----- double-double (multiprec.hpp:91-189) -----
+// Branch-free: both results are computed and selected, so the independent
+// re/im chains of complex arithmetic stay in one basic block and interleave
+// (a data-dependent branch here serialises them); same bits.
 PT_HD dd dd_norm(double h, double l) {  // multiprec.hpp:102-107
-  if (!finite(h)) return {h, 0.0};
   double e;
   double s = quick_two_sum(h, l, e);
-  return {s, e};
+  const bool f = finite(h);
+  return {f ? s : h, f ? e : 0.0};
 }
 PT_HD dd r_from(double x, dd*) { return {x, 0.0}; }
 PT_HD dd r_neg(dd a) { return {-a.hi, -a.lo}; }
@@ -266,14 +269,15 @@ PT_HD dd r_mul_d(dd a, double b) {  // multiprec.hpp:134-139
 }
 PT_HD dd r_div(dd a, dd b) {  // multiprec.hpp:145-155
   double q1 = div64(a.hi, b.hi);
-  if (!finite(q1)) return {q1, 0.0};
   dd r = r_sub(a, r_mul_d(b, q1));
   double q2 = div64(r.hi, b.hi);
   r = r_sub(r, r_mul_d(b, q2));
   double q3 = div64(r.hi, b.hi);
   double e;
   double s = quick_two_sum(q1, q2, e);
-  return r_add(dd{s, e}, dd{q3, 0.0});
+  const dd out = r_add(dd{s, e}, dd{q3, 0.0});
+  const bool f = finite(q1);  // non-finite first quotient: {q1, 0} (branch-free select)
+  return {f ? out.hi : q1, f ? out.lo : 0.0};
 }
 // Negative argument: the reference throws std::domain_error
 // (multiprec.hpp:178); the device returns NaN instead (never reached on the

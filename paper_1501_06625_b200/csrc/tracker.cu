@@ -42,7 +42,7 @@ inline int limbs(pt_prec p) { return p == PT_D ? 1 : (p == PT_DD ? 2 : 4); }
 // Per-path workspace layout (element counts); slice b of a batch starts at
 // b * dslice doubles / b * uslice u64 words.
 struct Layout {
-  long x, hist, ws, A, Rm, inv, rmaxp, hmod, scal, dx;  // double offsets
+  long x, hist, ws, A, Rm, inv, rmaxp, hmod, scal, dx, qg;  // double offsets
   long dslice;
   long flags, ctl, prof;  // u64 offsets
   long uslice;
@@ -66,6 +66,7 @@ Layout make_layout(int L, int n, int N, long ws_len) {
   o.hmod = take(N);
   o.scal = take(8);
   o.dx = take(2L * L * n);
+  o.qg = take((long)n * mgs_warp_qs(L, N));
   o.dslice = d;
   long u = 0;
   o.flags = u;
@@ -92,6 +93,7 @@ __host__ __device__ inline Work carve(double* dbase, unsigned long long* ubase, 
   W.hmod = d + o.hmod;
   W.scal = d + o.scal;
   W.dx = d + o.dx;
+  W.qg = d + o.qg;
   W.flags = u + o.flags;
   W.ctl = u + o.ctl;
   W.prof = u + o.prof;
@@ -552,7 +554,10 @@ int setup_cluster(pt_plan* p) {
   const void* fn = (const void*)&k_track_cluster<R>;
   PT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   p->cluster_size = 0;
+  const char* ce = getenv("PT_CLUSTER_MAX");  // tuning knob: cap the cluster size
+  const int cmax = ce ? atoi(ce) : 16;
   for (int c : {16, 8, 4, 2}) {
+    if (c > cmax) continue;
     int warp = 0;
     const size_t dyn = engine_smem(p->L, p->N, p->n, c, true, &warp);
     if (dyn == 0) continue;
@@ -604,6 +609,11 @@ int guarded(F&& f) {
   }
 }
 
+// the warp back substitution can stage R in the engine's dynamic smem
+int stage_fits(const pt_plan* p, size_t dyn_bytes) {
+  return backsub_stage_doubles(p->L, p->n) * 8 <= dyn_bytes ? 1 : 0;
+}
+
 template <class R>
 void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
   Work W = carve(p->dwork, p->uwork, p->lay, 0);
@@ -612,6 +622,7 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
     DevPlan dp = p->dp;
     dp.mgs_smem = p->cluster_dyn_smem > 0;
     dp.mgs_warp = p->cluster_warp;
+    dp.bs_smem = stage_fits(p, p->cluster_dyn_smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p->cluster_size);
     cfg.blockDim = dim3(kThreads);
@@ -630,6 +641,7 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
   DevPlan dp = p->dp;
   dp.mgs_smem = p->grid_dyn_smem > 0;
   dp.mgs_warp = p->grid_warp;
+  dp.bs_smem = stage_fits(p, p->grid_dyn_smem);
   pt_step_params spc = sp;
   TrackIO ioc = io;
   void* args[] = {&dp, &W, &spc, &ioc, &epoch};
@@ -1024,6 +1036,7 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   DevPlan bdp = p->dp;
   bdp.mgs_smem = p->batch_dyn_smem > 0;
   bdp.mgs_warp = p->batch_warp;
+  bdp.bs_smem = stage_fits(p, p->batch_dyn_smem);
   // launched as clusters of one CTA: the warp MGS pushes q_k with st.async,
   // which needs a cluster launch even when the cluster is the CTA itself
   cudaLaunchConfig_t cfg = {};

@@ -238,12 +238,13 @@ class TrackOutcome:
     t_end: float
     failure_kind: str
     trace: List[nat.TraceEvent] = field(default_factory=list)
+    solves: int = 0  # completed least-squares solves
 
     @staticmethod
     def from_native(end: np.ndarray, st: nat.PathStats, trace=None) -> "TrackOutcome":
         return TrackOutcome(st.status == 0, end, st.steps, st.accepted, st.newton_iters, st.start_iters,
                             st.final_residual, st.final_update, st.t_end,
-                            FAILURE_KINDS.get(st.failure_kind, str(st.failure_kind)), trace or [])
+                            FAILURE_KINDS.get(st.failure_kind, str(st.failure_kind)), trace or [], st.solves)
 
 
 class Homotopy:
