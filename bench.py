@@ -351,7 +351,8 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(h_start.numel() * 8),
                     "d2h_bytes_per_step": int(h_end.numel() * 8 + C.sizeof(nat.PathStats) * npaths),
                     "timing": "wall clock around the C-ABI call, max over ranks"},
-            "roofline": {"bound": "fp64-pipe", "kernel": "k_track_batch" if batch else "k_track_grid",
+            "roofline": {"bound": "fp64-pipe",
+                         "kernel": "k_track_batch" if batch else ("k_track_cluster" if hom.engine == "cluster" else "k_track_grid"),
                          "achieved": achieved * 1e-12, "peak": peak * 1e-12,
                          "unit": "T FP64-instr/s (DADD/DMUL/DFMA of the reference DD/QD algorithms; FMA = 1)",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
