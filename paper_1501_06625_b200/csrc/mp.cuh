@@ -353,10 +353,16 @@ PT_HDI qd qd_renorm5(double c0, double c1, double c2, double c3, double c4) {
 // qd_distill, multiprec.hpp:256-279, with K a compile-time constant so the
 // addend array lives in registers.  The reference orders addends by a stable
 // insertion sort on |m| (descending, ties keep input order); any stable sort
-// yields the same permutation.  This is that insertion sort, fully unrolled
-// with static indices and an early exit, comparing magnitudes as integers.
+// yields the same permutation.  Variants (PT_QD_SORT), all comparing
+// magnitudes as integers on the FP64 bits:
+//   3 (default) odd-even transposition: K rounds of adjacent compare-exchanges
+//     swapping only on strict <, branch-free, constant depth -- the lowest
+//     latency and the highest throughput measured on B200
+//     (tools/qd_sort_bench.cu: QD mul 6.6k cycles dependent, 3.6 T FP64 instr/s);
+//   2 insertion position by mask; 1 plain insertion; 0 insertion with a
+//     warp-uniform early exit.
 #ifndef PT_QD_SORT
-#define PT_QD_SORT 2
+#define PT_QD_SORT 3
 #endif
 template <int K>
 PT_HD qd qd_distill(double (&m)[K]) {
