@@ -126,6 +126,14 @@ PT_HD double bitsd(uint64_t b) {
 PT_HD uint64_t mag(double x) { return dbits(x) & 0x7fffffffffffffffull; }
 PT_HD bool finite(double x) { return (dbits(x) & 0x7ff0000000000000ull) != 0x7ff0000000000000ull; }
 PT_HD double fabs_(double x) { return bitsd(mag(x)); }
+// |a| < |b| as the reference writes it (std::fabs compare; false with NaN)
+PT_HD bool fabs_cmp_lt(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return ::fabs(a) < ::fabs(b);
+#else
+  return std::fabs(a) < std::fabs(b);
+#endif
+}
 PT_HD int clz32(unsigned x) {
 #if defined(__CUDA_ARCH__)
   return __clz(x);
@@ -354,15 +362,16 @@ PT_HDI qd qd_renorm5(double c0, double c1, double c2, double c3, double c4) {
 // addend array lives in registers.  The reference orders addends by a stable
 // insertion sort on |m| (descending, ties keep input order); any stable sort
 // yields the same permutation.  Variants (PT_QD_SORT), all comparing
-// magnitudes as integers on the FP64 bits:
-//   3 (default) odd-even transposition: K rounds of adjacent compare-exchanges
-//     swapping only on strict <, branch-free, constant depth -- the lowest
-//     latency and the highest throughput measured on B200
-//     (tools/qd_sort_bench.cu: QD mul 6.6k cycles dependent, 3.6 T FP64 instr/s);
+//   4 (default) odd-even transposition: K rounds of adjacent compare-exchanges
+//     swapping only on strict fabs(a) < fabs(b) (the reference's compare, one
+//     DSETP), branch-free, constant depth -- lowest latency and highest
+//     throughput measured on B200 (tools/qd_sort_bench.cu: QD mul 3.3k cycles
+//     dependent, 5.6 T FP64 instr/s; the integer-key variant 3: 5.0k, 3.6 T);
+//   3 the same network comparing magnitudes as integers on the FP64 bits;
 //   2 insertion position by mask; 1 plain insertion; 0 insertion with a
-//     warp-uniform early exit.
+//     warp-uniform early exit (integer keys).
 #ifndef PT_QD_SORT
-#define PT_QD_SORT 3
+#define PT_QD_SORT 4
 #endif
 template <int K>
 PT_HD qd qd_distill(double (&m)[K]) {
@@ -384,6 +393,21 @@ PT_HD qd qd_distill(double (&m)[K]) {
 #pragma unroll
     for (int j = i; j >= 1; --j) m[j] = (j > pos) ? m[j - 1] : (j == pos ? v : m[j]);
     if (pos == 0) m[0] = v;
+  }
+#elif PT_QD_SORT == 4
+  // odd-even transposition with the reference's own comparison,
+  // fabs(m[i]) < fabs(m[i+1]) (one DSETP with |.| operand modifiers on the
+  // otherwise idle FP64 pipe instead of 64-bit integer compares on the ALU
+  // pipe); NaN never swaps, exactly as it blocks the reference's insertion.
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+#pragma unroll
+    for (int i = r & 1; i + 1 < K; i += 2) {
+      const double a = m[i], b = m[i + 1];
+      const bool sw = fabs_cmp_lt(a, b);
+      m[i] = sw ? b : a;
+      m[i + 1] = sw ? a : b;
+    }
   }
 #elif PT_QD_SORT == 3
   // odd-even transposition sort: K rounds of adjacent compare-exchanges that
