@@ -58,12 +58,16 @@ __device__ __forceinline__ cplx<R> shfl0(const cplx<R>& v, int src) {
   return {shfl0(v.re, src), shfl0(v.im, src)};
 }
 
+// width_mgs(N) as a function of E = ceil(N/32): 32 for N <= 64, 64 for N <= 128
+template <int E>
+constexpr int kCanonP = E <= 2 ? 32 : 64;
+
 // Canonical width-P sum (P = width_mgs(N) in {32, 64}) of the values v[r]
 // of rows lane + 32 r; the result is valid in lane 0.
 template <class T, int E>
 __device__ __forceinline__ T warp_canon(const T (&v)[E], int lane, int N, int P) {
   T acc = v[0];
-  if (P == 32) {
+  if (P == 32) {  // compile-time at every call site (kCanonP<E>)
 #pragma unroll
     for (int r = 1; r < E; ++r) acc = pick(lane + 32 * r < N, add_v(acc, v[r]), acc);
   } else {  // P == 64 (65 <= N <= 128): partial l = c[l] + c[l+64], partial l+32 = c[l+32] + c[l+96]
@@ -229,7 +233,7 @@ struct WarpMgs {
     R v[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) v[r] = c_norm_sqr(a[r]);  // rows >= N never enter the sum
-    const R nrm2 = warp_canon(v, lane, N, P.P_mgs);
+    const R nrm2 = warp_canon(v, lane, N, kCanonP<E>);
     int ok = 0;
     R inv = rconst<R>(0.0);
     double mx = 0.0;
@@ -275,7 +279,7 @@ struct WarpMgs {
     cplx<R> v[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) v[r] = c_conj_mul(q[r], a[r]);  // rows >= N never enter the sum
-    cplx<R> rkj = warp_canon(v, lane, N, P.P_mgs);
+    cplx<R> rkj = warp_canon(v, lane, N, kCanonP<E>);
     if (lane == 0) store_c<R>(W.Rm, SR, (long)j * n + k, rkj);
     rkj = shfl0(rkj, 0);
     if (j < n || k < n - 1) {

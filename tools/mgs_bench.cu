@@ -13,7 +13,7 @@
 using namespace ptdev;
 using R = dd;
 
-__global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* A0, int reps, double* out) {
+__global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* A0, int reps, double* out, int probe) {
   __shared__ Smem<R> sh;
   __shared__ uint32_t s_flags[kMaxCols];
   extern __shared__ double dyn[];
@@ -35,6 +35,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* 
       W.A[q] = A0[q];
     team.sync(&sh.flag);
     if (r == 1) t0 = gtimer();
+    if (probe && team.block == 0 && threadIdx.x >= 192 && threadIdx.x < 224) {
+      // concurrent probe: warp 6 of CTA 0 (no columns) runs the isolated
+      // projection loop on a private smem slot while the MGS runs
+      const int lane = threadIdx.x & 31;
+      const WarpMgs<R, ClusterTeam> m{P, W, team, sh, dyn, ColMap{team.nblocks, P.mgs_B}, lane, 6, P.N, P.n, SA,
+                                      (long)P.n * (P.n + 1), 2L * L * P.N, 1ull, 0x1p-52, nullptr, nullptr};
+      cplx<R> q[2], a[2];
+      for (int rr = 0; rr < 2; ++rr) q[rr] = cplx<R>{{0.5 + 1e-4 * lane, 1e-20}, {0.25, 0}};
+      double* scratch = dyn + 6 * 4 * 64;  // slot of warp 6 (no columns)
+      long long c0 = clock64();
+      for (int i = 0; i < 64; ++i) m.template project<2>(3, 10, q, a, scratch);
+      long long c1 = clock64();
+      if (lane == 0 && r == reps - 1) out[2] = (double)(c1 - c0) / 64 + (a[0].re.hi == 12345.0);
+    } else
     mgs_warp<R, ClusterTeam>(P, W, team, sh, dyn, 1000ull + r, 0x1p-52);
     team.sync(&sh.flag);
     if (threadIdx.x == 0) ++sh.mgs_seq;
@@ -107,11 +121,13 @@ int main(int argc, char** argv) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_mgs, P, W, A0, reps, out);
+  const int probe = argc > 5 ? atoi(argv[5]) : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_mgs, P, W, A0, reps, out, probe);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  double ns = 0, iso = 0;
+  double ns = 0, iso = 0, conc = 0;
   cudaMemcpy(&ns, out, 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(&iso, out + 1, 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&conc, out + 2, 8, cudaMemcpyDeviceToHost);
   std::vector<unsigned long long> t(6 * (n + 2));
   cudaMemcpy(t.data(), prof + 8, t.size() * 8, cudaMemcpyDeviceToHost);
   std::vector<double> wl, pr, no, col;
@@ -121,9 +137,13 @@ int main(int argc, char** argv) {
     no.push_back((double)(t[6 * j + 4] - t[6 * j + 3]));
     col.push_back((double)(t[6 * j + 5] - t[6 * (j - 1) + 5]));
   }
+  if (getenv("MGS_DUMP")) {
+    for (size_t q = 0; q < pr.size(); ++q) printf("%d:%.0f/%.0f ", (int)q + 2, pr[q], no[q]);
+    printf("\n");
+  }
   auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v.empty() ? 0.0 : v[v.size() / 2]; };
   printf("{\"err\": \"%s\", \"N\": %d, \"C\": %d, \"B\": %d, \"ns_per_mgs\": %.0f, \"wait_load_cyc\": %.0f, "
-         "\"project_cyc\": %.0f, \"normalize_cyc\": %.0f, \"column_ns\": %.0f, \"isolated_project_cyc\": %.0f}\n",
-         cudaGetErrorString(e), N, C, B, ns, med(wl), med(pr), med(no), med(col), iso);
+         "\"project_cyc\": %.0f, \"normalize_cyc\": %.0f, \"column_ns\": %.0f, \"isolated_project_cyc\": %.0f, \"concurrent_probe_cyc\": %.0f}\n",
+         cudaGetErrorString(e), N, C, B, ns, med(wl), med(pr), med(no), med(col), iso, conc);
   return 0;
 }

@@ -31,3 +31,5 @@ out = {"workload": w.name, "engine": hom.engine, "per_column_median": {
     "column_ns (q_{j-1} pushed -> q_j pushed)": med([t[j, 5] - t[j - 1, 5] for j in cols])},
     "total_ns": float(t[n - 1, 5] - t[1, 0])}
 print(json.dumps(out))
+if os.environ.get("MGS_DUMP"):
+    print(" ".join(f"{j}:{int(t[j, 3] - t[j, 2])}/{int(t[j, 4] - t[j, 3])}" for j in cols))
