@@ -162,6 +162,9 @@ int pt_microbench(int device, int32_t what, double* out);
  * [2] MGS, [3] back substitution + update, [4] predictor, [5] Newton
  * iterations (count); reset != 0 clears them. */
 int pt_plan_profile(pt_plan* plan, double* out, int32_t reset);
+/* The same timers of batch CTA `slice` (k_track_batch, accumulated over the
+ * paths that CTA tracked). */
+int pt_plan_batch_profile(pt_plan* plan, int32_t slice, double* out, int32_t reset);
 
 /* MGS timeline of the last single-path launch (debugging aid): for column j,
  * out[3j..3j+2] = globaltimer ns when q_{j-1} reached the owner of column j,

@@ -87,6 +87,7 @@ PROTOTYPES = {
     "pt_plan_work": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
     "pt_fp64_peak": (C.c_int, [C.c_int, _dp, _dp]),
     "pt_plan_profile": (C.c_int, [_vp, _dp, C.c_int32]),
+    "pt_plan_batch_profile": (C.c_int, [_vp, C.c_int32, _dp, C.c_int32]),
     "pt_plan_mgs_timeline": (C.c_int, [_vp, _dp, C.c_int32]),
     "pt_microbench": (C.c_int, [C.c_int, C.c_int32, _dp]),
     "pt_plan_get_trace": (C.c_int, [_vp, C.POINTER(TraceEvent), C.c_int32, C.POINTER(C.c_int32)]),

@@ -326,6 +326,21 @@ template <class R>
 __device__ __forceinline__ cplx<R> shfl_down_r(const cplx<R>& v, int off) {
   return {shfl_down_r(v.re, off), shfl_down_r(v.im, off)};
 }
+__device__ __forceinline__ double shfl0(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ dd shfl0(dd v, int src) {
+  return {__shfl_sync(0xffffffffu, v.hi, src), __shfl_sync(0xffffffffu, v.lo, src)};
+}
+__device__ __forceinline__ qd shfl0(const qd& v, int src) {
+  qd r;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) r.c[l] = __shfl_sync(0xffffffffu, v.c[l], src);
+  return r;
+}
+template <class R>
+__device__ __forceinline__ cplx<R> shfl0(const cplx<R>& v, int src) {
+  return {shfl0(v.re, src), shfl0(v.im, src)};
+}
+
 __device__ __forceinline__ double add_v(double a, double b) { return add64(a, b); }
 __device__ __forceinline__ dd add_v(dd a, dd b) { return r_add(a, b); }
 __device__ __forceinline__ qd add_v(const qd& a, const qd& b) { return r_add(a, b); }
@@ -497,19 +512,43 @@ __device__ __noinline__ void eval_monomials(const DevPlan& P, const Work& W, int
   }
 }
 
+// One contribution: coef * (monomial value or partial), or the coefficient
+// itself for a constant term (wi < 0).  Branch-free so unrolled copies
+// interleave.
+template <class R>
+__device__ __forceinline__ cplx<R> contrib(const DevPlan& P, const Work& W, int ci, int wi) {
+  const cplx<R> c = load_c<R>(P.coef, P.n_coef, ci);
+  const cplx<R> m = load_c<R>(W.ws, P.ws_len, wi < 0 ? 0 : wi);
+  return pick(wi < 0, c, c_mul(c, m));
+}
+
 // Canonical sum of one contribution list by a group; valid at g.p == 0.
+// Partial p = c[p] + c[p+Pw] + ... is accumulated in order, kU contributions
+// per round: their index and value loads and products are independent, so
+// the L2 round trips overlap and only the additions stay sequential.
 template <class R>
 __device__ __forceinline__ cplx<R> slot_sum(const DevPlan& P, const Work& W, const Group& g, int beg, int K, cplx<R>* sm) {
+  constexpr int kU = limbs_of<R>::L == 4 ? 2 : 4;
   const int Pw = width_eval_d(K);
   cplx<R> acc = c_zero<R>();
   if (g.p < Pw && g.p < K) {
-    for (int r = g.p; r < K; r += Pw) {
-      const int ci = P.ctr_coef[beg + r];
-      const int wi = P.ctr_ws[beg + r];
-      const cplx<R> c = load_c<R>(P.coef, P.n_coef, ci);
-      const cplx<R> v = wi < 0 ? c : c_mul(c, load_c<R>(W.ws, P.ws_len, wi));
-      acc = (r == g.p) ? v : c_add(acc, v);
+    int r = g.p;
+    acc = contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]);
+    r += Pw;
+    for (; r + (kU - 1) * Pw < K; r += kU * Pw) {
+      int ci[kU], wi[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        ci[u] = P.ctr_coef[beg + r + u * Pw];
+        wi[u] = P.ctr_ws[beg + r + u * Pw];
+      }
+      cplx<R> v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = contrib<R>(P, W, ci[u], wi[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc = c_add(acc, v[u]);
     }
+    for (; r < K; r += Pw) acc = c_add(acc, contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]));
   }
   return group_tree(acc, g, Pw, K, sm);
 }

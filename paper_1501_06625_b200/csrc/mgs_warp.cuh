@@ -43,21 +43,6 @@ struct ColMap {
   }
 };
 
-__device__ __forceinline__ double shfl0(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
-__device__ __forceinline__ dd shfl0(dd v, int src) {
-  return {__shfl_sync(0xffffffffu, v.hi, src), __shfl_sync(0xffffffffu, v.lo, src)};
-}
-__device__ __forceinline__ qd shfl0(const qd& v, int src) {
-  qd r;
-#pragma unroll
-  for (int l = 0; l < 4; ++l) r.c[l] = __shfl_sync(0xffffffffu, v.c[l], src);
-  return r;
-}
-template <class R>
-__device__ __forceinline__ cplx<R> shfl0(const cplx<R>& v, int src) {
-  return {shfl0(v.re, src), shfl0(v.im, src)};
-}
-
 // width_mgs(N) as a function of E = ceil(N/32): 32 for N <= 64, 64 for N <= 128
 template <int E>
 constexpr int kCanonP = E <= 2 ? 32 : 64;

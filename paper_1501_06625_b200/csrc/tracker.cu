@@ -149,8 +149,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   team.sync(&sh.flag);  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
+// Batch CTAs per SM: two paths share an SM in D / DD (128 registers per
+// thread suffice there); QD keeps the whole register file for one path.
 template <class R>
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kBatchCtasPerSm = limbs_of<R>::L == 4 ? 1 : 2;
+
+template <class R>
+__global__ void __launch_bounds__(kThreads, kBatchCtasPerSm<R>)
     k_track_batch(DevPlan P, double* dbase, unsigned long long* ubase, Layout lay, pt_step_params sp,
                   const double* starts, double* ends, pt_path_stats* stats, int n_paths,
                   unsigned long long* queue, unsigned long long epoch_base) {
@@ -882,6 +887,19 @@ int pt_plan_profile(pt_plan* p, double* out, int32_t reset) {
   PT_CUDA(cudaSetDevice(p->device));
   PT_CUDA(cudaStreamSynchronize(p->stream));
   unsigned long long* prof = carve(p->dwork, p->uwork, p->lay, 0).prof;
+  unsigned long long h[kProfSlots];
+  PT_CUDA(cudaMemcpy(h, prof, sizeof h, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < kProfSlots; ++i) out[i] = (double)h[i];
+  if (reset) PT_CUDA(cudaMemset(prof, 0, sizeof h));
+  return PT_OK;
+}
+
+int pt_plan_batch_profile(pt_plan* p, int32_t slice, double* out, int32_t reset) {
+  if (!p || !out || slice < 0) return PT_E_INVAL;
+  if (!p->bu || slice >= p->batch_blocks) return fail(PT_E_INVAL, "no such batch workspace slice");
+  PT_CUDA(cudaSetDevice(p->device));
+  PT_CUDA(cudaStreamSynchronize(p->stream));
+  unsigned long long* prof = carve(p->bwork, p->bu, p->lay, slice).prof;
   unsigned long long h[kProfSlots];
   PT_CUDA(cudaMemcpy(h, prof, sizeof h, cudaMemcpyDeviceToHost));
   for (int i = 0; i < kProfSlots; ++i) out[i] = (double)h[i];
