@@ -553,19 +553,29 @@ __device__ __forceinline__ cplx<R> slot_sum(const DevPlan& P, const Work& W, con
   return group_tree(acc, g, Pw, K, sm);
 }
 
-// Width-32 canonical sum of K <= KMAX contributions evaluated by one lane:
-// partial p = c[p]; levels off = 4, 2, 1 (the only ones with p + off < K).
+// Canonical width-32 sum of K <= 512 contributions by ONE lane (lane tasks).
+// Leaves are the partials p = c[p] + c[p+32] + ... (each summed in order);
+// visiting them in 5-bit bit-reversed order p = brev(t) and merging the two
+// top entries of a small stack after every leaf whose count t+1 is a multiple
+// of 2, 4, ... reproduces the tree exactly: the first merges are
+// (c0 + c16), (c8 + c24), then (c0+c16) + (c8+c24) = level 8, and so on, each
+// merge being partial[p] += partial[p+off] with the lower index on the left.
+// An empty right subtree (its least index p+off >= K) is skipped, exactly the
+// "p + off < K" rule.  Stack positions depend only on t: fully unrolled, the
+// stack lives in registers.  No shuffles, no idle lanes.
+__host__ __device__ constexpr int brev5(int t) {
+  return ((t & 1) << 4) | ((t & 2) << 2) | (t & 4) | ((t & 8) >> 2) | ((t & 16) >> 4);
+}
+__host__ __device__ constexpr int popc5(int t) { return (t & 1) + ((t >> 1) & 1) + ((t >> 2) & 1) + ((t >> 3) & 1) + ((t >> 4) & 1); }
+__host__ __device__ constexpr int ctz6(int x) { return (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : (x & 8) ? 3 : (x & 16) ? 4 : 5; }
+
+// K <= KMAX: all contributions in registers, levels off = 4, 2, 1 only.
 template <class R, int KMAX>
 __device__ __forceinline__ cplx<R> lane_sum(const DevPlan& P, const Work& W, int beg, int K) {
   cplx<R> part[KMAX];
 #pragma unroll
   for (int r = 0; r < KMAX; ++r) {
-    if (r < K) {
-      const int ci = P.ctr_coef[beg + r];
-      const int wi = P.ctr_ws[beg + r];
-      const cplx<R> c = load_c<R>(P.coef, P.n_coef, ci);
-      part[r] = wi < 0 ? c : c_mul(c, load_c<R>(W.ws, P.ws_len, wi));
-    }
+    if (r < K) part[r] = contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]);
   }
 #pragma unroll
   for (int off = KMAX / 2; off >= 1; off >>= 1) {
@@ -574,6 +584,32 @@ __device__ __forceinline__ cplx<R> lane_sum(const DevPlan& P, const Work& W, int
       if (p + off < K) part[p] = c_add(part[p], part[p + off]);
   }
   return part[0];
+}
+
+template <class R>
+__device__ __forceinline__ cplx<R> lane_canon32(const DevPlan& P, const Work& W, int beg, int K) {
+  cplx<R> st[6];
+  bool ne[6];
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const int p = brev5(t);
+    const int d = popc5(t);  // stack depth before this leaf
+    cplx<R> v = c_zero<R>();
+    const bool has = p < K;
+    if (has) {
+      v = contrib<R>(P, W, P.ctr_coef[beg + p], P.ctr_ws[beg + p]);
+      for (int r = p + 32; r < K; r += 32) v = c_add(v, contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]));
+    }
+    st[d] = v;
+    ne[d] = has;
+    // merges after leaf t: as many as trailing zeros of t + 1
+#pragma unroll
+    for (int m = 0; m < ctz6(t + 1); ++m) {
+      const int top = d - m;
+      if (ne[top]) st[top - 1] = c_add(st[top - 1], st[top]);
+    }
+  }
+  return st[0];
 }
 
 template <class R>
@@ -601,21 +637,21 @@ __device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const T
   R wT;
   weights<R>(P, t, wS, wT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {  // lane tasks: one small slot per lane
+  {  // lane tasks: one slot per lane (canonical width 32, K <= lane_k)
     constexpr int KM = limbs_of<R>::L == 4 ? 4 : 8;
     const int beg = P.class_beg[0], end = P.class_beg[1];
     const int nth = team.nblocks * kThreads;
     for (int ti = beg + team.block * kThreads + threadIdx.x; ti < end; ti += nth) {
       const ptplan::SlotTask tk = P.tasks[ti];
       cplx<R> Sg = c_zero<R>(), Sf;
-      if (tk.g_cnt > 0) Sg = lane_sum<R, KM>(P, W, tk.g_beg, tk.g_cnt);
+      if (tk.g_cnt > 0) Sg = tk.g_cnt <= KM ? lane_sum<R, KM>(P, W, tk.g_beg, tk.g_cnt) : lane_canon32<R>(P, W, tk.g_beg, tk.g_cnt);
       bool have_f;
       if (tk.f_cnt < 0) {
         Sf = Sg;
         have_f = tk.g_cnt > 0;
       } else {
         Sf = c_zero<R>();
-        if (tk.f_cnt > 0) Sf = lane_sum<R, KM>(P, W, tk.f_beg, tk.f_cnt);
+        if (tk.f_cnt > 0) Sf = tk.f_cnt <= KM ? lane_sum<R, KM>(P, W, tk.f_beg, tk.f_cnt) : lane_canon32<R>(P, W, tk.f_beg, tk.f_cnt);
         have_f = tk.f_cnt > 0;
       }
       slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);

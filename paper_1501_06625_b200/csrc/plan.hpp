@@ -54,10 +54,15 @@ struct SlotTask {
   int32_t pad;
 };
 
-// Tasks whose sums have at most kLaneK(L) contributions on each side run one
-// per lane (the width-32 canonical tree then only has its off = 4, 2, 1
-// levels, evaluated sequentially by that lane: same shape, same bits).
+// Tasks whose sums have at most lane_k contributions on each side run one per
+// lane: lane_canon32 (device.cuh) evaluates the width-32 canonical tree of any
+// K <= 512 sequentially in one lane -- same shape, same bits.  Two partitions
+// of the same tasks: the single-path engines are latency bound and keep only
+// short sums on lanes; the batch kernel (one path per CTA, many CTAs) is
+// throughput bound and runs everything up to 128 contributions on lanes, so
+// no lane idles through a warp tree of a short sum.
 inline int lane_k(int L) { return L == 4 ? 4 : 8; }
+inline int lane_k_batch(int L) { return L == 4 ? 4 : 128; }
 
 struct HostPlan {
   int n = 0, N = 0, L = 1;
@@ -67,6 +72,8 @@ struct HostPlan {
   // slots
   std::vector<SlotTask> tasks;
   int32_t class_beg[6] = {0, 0, 0, 0, 0, 0};  // lane tasks, then gw = 8,4,2,1
+  std::vector<SlotTask> tasks_b;                // batch partition (lane_k_batch)
+  int32_t class_beg_b[6] = {0, 0, 0, 0, 0, 0};
   std::vector<int32_t> ctr_coef, ctr_ws;
   // coefficients of all terms of g then f, complex SoA [2][L][n_coef]
   std::vector<double> coef;
@@ -257,19 +264,27 @@ inline HostPlan compile(const pt_system_desc* g, const pt_system_desc* f, int L)
         if (tk.f_cnt > 0) w = std::max(w, width_eval(tk.f_cnt));
       }
       check(P.ctr_coef.size() < ((size_t)1 << 31), "too many contributions");
-      tk.gw = w / 32;
-      if (tk.g_cnt <= lane_k(L) && (tk.f_cnt < 0 || tk.f_cnt <= lane_k(L))) tk.gw = 0;
+      tk.gw = w / 32;  // group width in warps when not a lane task
       tasks.push_back(tk);
     }
   }
   // group tasks by class (lane tasks, then 8, 4, 2, 1 warps); stable within a class
   const int classes[5] = {0, 8, 4, 2, 1};
-  for (int c = 0; c < 5; ++c) {
-    P.class_beg[c] = (int32_t)P.tasks.size();
-    for (auto& tk : tasks)
-      if (tk.gw == classes[c]) P.tasks.push_back(tk);
-  }
-  P.class_beg[5] = (int32_t)P.tasks.size();
+  auto partition = [&](int lk, std::vector<SlotTask>& out, int32_t* cb) {
+    for (int c = 0; c < 5; ++c) {
+      cb[c] = (int32_t)out.size();
+      for (const auto& tk : tasks) {
+        const bool lane = tk.g_cnt <= lk && (tk.f_cnt < 0 || tk.f_cnt <= lk);
+        if ((lane ? 0 : tk.gw) == classes[c]) {
+          out.push_back(tk);
+          out.back().gw = lane ? 0 : tk.gw;
+        }
+      }
+    }
+    cb[5] = (int32_t)out.size();
+  };
+  partition(lane_k(L), P.tasks, P.class_beg);
+  partition(lane_k_batch(L), P.tasks_b, P.class_beg_b);
   if (P.ctr_coef.empty()) {
     P.ctr_coef.push_back(0);
     P.ctr_ws.push_back(-1);

@@ -438,6 +438,8 @@ struct pt_plan {
   int grid_blocks = 1;
   size_t grid_dyn_smem = 0;   // dynamic smem of k_track_grid / k_eval
   int grid_warp = 0, cluster_warp = 0, batch_warp = 0;  // warp-per-column MGS per engine
+  const ptplan::SlotTask* tasks_b = nullptr;            // batch partition of the slot tasks
+  int class_beg_b[6] = {0, 0, 0, 0, 0, 0};
   int engine = 0;             // 0 grid, 1 cluster (single path)
   int cluster_size = 0;       // CTAs of the cluster engine (0: unavailable)
   size_t cluster_dyn_smem = 0;
@@ -733,7 +735,8 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
         {hp.mono_var.data(), hp.mono_var.size() * 4},   {hp.mono_exp.data(), hp.mono_exp.size() * 4},
         {hp.tasks.data(), hp.tasks.size() * sizeof(ptplan::SlotTask)},
         {hp.ctr_coef.data(), hp.ctr_coef.size() * 4},   {hp.ctr_ws.data(), hp.ctr_ws.size() * 4},
-        {hp.coef.data(), hp.coef.size() * 8},           {gamma, (size_t)2 * L * 8}};
+        {hp.coef.data(), hp.coef.size() * 8},           {gamma, (size_t)2 * L * 8},
+        {hp.tasks_b.data(), hp.tasks_b.size() * sizeof(ptplan::SlotTask)}};
     size_t total = 0;
     std::vector<size_t> offs;
     for (auto& pc : pieces) {
@@ -762,6 +765,8 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     dp.ws_len = hp.ws_len;
     dp.tasks = (const ptplan::SlotTask*)(base + offs[6]);
     for (int c = 0; c < 6; ++c) dp.class_beg[c] = hp.class_beg[c];
+    p->tasks_b = (const ptplan::SlotTask*)(base + offs[11]);
+    for (int c = 0; c < 6; ++c) p->class_beg_b[c] = hp.class_beg_b[c];
     dp.ctr_coef = (const int32_t*)(base + offs[7]);
     dp.ctr_ws = (const int32_t*)(base + offs[8]);
     dp.coef = (const double*)(base + offs[9]);
@@ -1055,6 +1060,8 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   bdp.mgs_smem = p->batch_dyn_smem > 0;
   bdp.mgs_warp = p->batch_warp;
   bdp.bs_smem = stage_fits(p, p->batch_dyn_smem);
+  bdp.tasks = p->tasks_b;
+  for (int c = 0; c < 6; ++c) bdp.class_beg[c] = p->class_beg_b[c];
   // launched as clusters of one CTA: the warp MGS pushes q_k with st.async,
   // which needs a cluster launch even when the cluster is the CTA itself
   cudaLaunchConfig_t cfg = {};
