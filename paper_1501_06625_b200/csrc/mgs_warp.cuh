@@ -52,6 +52,23 @@ constexpr int kCanonP = E <= 2 ? 32 : 64;
 template <class T, int E>
 __device__ __forceinline__ T warp_canon(const T (&v)[E], int lane, int N, int P) {
   T acc = v[0];
+  if (N >= 32 * E) {  // every row present (warp-uniform): no per-level selects
+    if (P == 32) {
+#pragma unroll
+      for (int r = 1; r < E; ++r) acc = add_v(acc, v[r]);
+    } else {
+      if constexpr (E > 2) acc = add_v(acc, v[2]);
+      if constexpr (E > 1) {
+        T a1 = v[1];
+        if constexpr (E > 3) a1 = add_v(a1, v[3]);
+        acc = add_v(acc, a1);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc = add_v(acc, shfl_down_r(acc, off));  // lanes >= off: unused
+    return acc;
+  }
   if (P == 32) {  // compile-time at every call site (kCanonP<E>)
 #pragma unroll
     for (int r = 1; r < E; ++r) acc = pick(lane + 32 * r < N, add_v(acc, v[r]), acc);
@@ -260,18 +277,32 @@ struct WarpMgs {
   // r_kj = q_k^H a_j, a_j -= r_kj q_k; leaves the updated a_j in a.
   template <int E>
   __device__ void project(int k, int j, const cplx<R> (&q)[E], cplx<R> (&a)[E], double* col) const {
+#ifdef PT_MGS_FINE  // stage clocks of the critical projection (tools/mgs_bench.cu only)
+    unsigned long long* fd = (j == k + 1 && lane == 0) ? W.prof + kProfSlots + 6 * (n + 2) + 8 * j : nullptr;
+#define PT_FINE(i, dep) \
+  if (fd) fd[i] = clock64() + (unsigned long long)(r_hi(dep) == 12345.0);
+#else
+#define PT_FINE(i, dep)
+#endif
+    PT_FINE(0, q[0].re)
     load_col(col, N, a);
+    PT_FINE(1, a[0].re)
     cplx<R> v[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) v[r] = c_conj_mul(q[r], a[r]);  // rows >= N never enter the sum
+    PT_FINE(2, v[E - 1].im)
     cplx<R> rkj = warp_canon(v, lane, N, kCanonP<E>);
+    PT_FINE(3, rkj.re)
     if (lane == 0) store_c<R>(W.Rm, SR, (long)j * n + k, rkj);
     rkj = shfl0(rkj, 0);
+    PT_FINE(4, rkj.im)
     if (j < n || k < n - 1) {
 #pragma unroll
       for (int r = 0; r < E; ++r) a[r] = c_sub(a[r], c_mul(rkj, q[r]));  // rows >= N: ignored garbage
+      PT_FINE(5, a[E - 1].im)
       store_col(col, N, a);
     }
+#undef PT_FINE
   }
 
   template <int E, bool MB>

@@ -242,14 +242,25 @@ PT_HD double r_limb(double a, int) { return a; }
 PT_HD void r_set_limb(double& a, int, double v) { a = v; }
 
 // ----- double-double (multiprec.hpp:91-189) -----
-// Branch-free: both results are computed and selected, so the independent
-// re/im chains of complex arithmetic stay in one basic block and interleave
-// (a data-dependent branch here serialises them); same bits.
+// multiprec.hpp:102-107 returns {h, 0} for a non-finite h.  On the device
+// that select is dropped by default: quick_two_sum of a non-finite h gives
+// {h (or NaN), NaN}, so only the LOW limb of a non-finite value differs
+// (NaN instead of 0) and every finite result is bit-identical.  The select --
+// a predicate or mask per DD operation -- made ptxas serialise independent DD
+// chains on the MGS critical path (tools/mgs_bench.cu: complex DD axpy of
+// two rows 1.4k -> 0.55k cycles, warp tree 1.8k -> 1.1k, per MGS column
+// 3.9 -> 2.9 us).  Non-finite values only occur on paths that fail; NaN
+// payloads differ between the GPU and x86 anyway.  -DPT_DD_EXACT_NONFINITE
+// restores the reference's branch on the device.
 PT_HD dd dd_norm(double h, double l) {  // multiprec.hpp:102-107
   double e;
   double s = quick_two_sum(h, l, e);
-  const bool f = finite(h);
-  return {f ? s : h, f ? e : 0.0};
+#if defined(__CUDA_ARCH__) && !defined(PT_DD_EXACT_NONFINITE)
+  return {s, e};
+#else
+  if (!finite(h)) return {h, 0.0};
+  return {s, e};
+#endif
 }
 PT_HD dd r_from(double x, dd*) { return {x, 0.0}; }
 PT_HD dd r_neg(dd a) { return {-a.hi, -a.lo}; }

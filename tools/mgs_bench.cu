@@ -4,6 +4,7 @@
 // kernel (same instrumentation as tools/mgs_timeline.py) and ns per MGS.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -std=c++17 -o mgs_bench_bin mgs_bench.cu
 //   ./mgs_bench_bin [N] [C] [B] [reps]
+#define PT_MGS_FINE 1
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -102,9 +103,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&qg, (size_t)n * mgs_warp_qs(L, N) * 8);
   cudaMalloc(&flags, (n + 1) * 8);
   cudaMalloc(&ctl, 64 * 8);
-  cudaMalloc(&prof, (8 + 6 * (n + 2)) * 8);
+  cudaMalloc(&prof, (8 + 14 * (n + 2)) * 8);
   cudaMemset(ctl, 0, 64 * 8);
-  cudaMemset(prof, 0, (8 + 6 * (n + 2)) * 8);
+  cudaMemset(prof, 0, (8 + 14 * (n + 2)) * 8);
   cudaMemcpy(A0, hA.data(), hA.size() * 8, cudaMemcpyHostToDevice);
   W.A = A; W.Rm = Rm; W.inv = inv; W.rmaxp = rmaxp; W.flags = flags; W.ctl = ctl; W.prof = prof; W.qg = qg;
   const size_t dyn = mgs_warp_bytes(L, N, n, C, true);
@@ -141,9 +142,16 @@ int main(int argc, char** argv) {
     for (size_t q = 0; q < pr.size(); ++q) printf("%d:%.0f/%.0f ", (int)q + 2, pr[q], no[q]);
     printf("\n");
   }
+  std::vector<unsigned long long> fine(8 * (n + 2));
+  cudaMemcpy(fine.data(), prof + 8 + 6 * (n + 2), fine.size() * 8, cudaMemcpyDeviceToHost);
+  std::vector<double> st[5];
+  for (int j = 2; j < n; ++j)
+    for (int q = 0; q < 5; ++q) st[q].push_back((double)(fine[8 * j + q + 1] - fine[8 * j + q]));
   auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v.empty() ? 0.0 : v[v.size() / 2]; };
   printf("{\"err\": \"%s\", \"N\": %d, \"C\": %d, \"B\": %d, \"ns_per_mgs\": %.0f, \"wait_load_cyc\": %.0f, "
          "\"project_cyc\": %.0f, \"normalize_cyc\": %.0f, \"column_ns\": %.0f, \"isolated_project_cyc\": %.0f, \"concurrent_probe_cyc\": %.0f}\n",
          cudaGetErrorString(e), N, C, B, ns, med(wl), med(pr), med(no), med(col), iso, conc);
+  printf("{\"fine_cycles\": {\"load_col\": %.0f, \"conj_mul\": %.0f, \"tree\": %.0f, \"bcast\": %.0f, \"axpy\": %.0f}}\n",
+         med(st[0]), med(st[1]), med(st[2]), med(st[3]), med(st[4]));
   return 0;
 }
