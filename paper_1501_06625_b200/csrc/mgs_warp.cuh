@@ -154,8 +154,11 @@ template <class R, class Team>
 struct WarpMgs {
   static constexpr int L = limbs_of<R>::L;
   const DevPlan& P;
-  const Work& W;
-  const Team& team;
+  // Work and Team by value: through references every store to shared or
+  // global memory may alias them, so their pointers would be reloaded (from
+  // the kernel's stack) on the critical chain after each store.
+  const Work W;
+  const Team team;
   Smem<R>& sh;
   double* colsm;  // this CTA's dynamic smem (layout above)
   ColMap cm;
