@@ -42,6 +42,7 @@ enum { NW_OK = 0, NW_RESIDUAL_INCREASE = 1, NW_ITERATION_BUDGET = 2, NW_LINEAR_S
 
 struct DevPlan {
   int n, N, M;
+  int mono_long;  // leading monomials (size >= kMonoSplit) evaluated by lane pairs
   int P_mgs;   // canonical width of the MGS sums
   int mgs_gw;  // warps per MGS group (>= P_mgs/32; one element per thread when N <= 256)
   const int32_t* mono_size;
@@ -458,10 +459,99 @@ __device__ void weights(const DevPlan& P, double t, cplx<R>& wS, R& wT) {
 // Reverse-mode value + partials of every monomial.
 // Prefix products F[j] are parked in the slot of partial j+1 and consumed by
 // the backward sweep, so the workspace is the only scratch.
+
+// Exponents >= 2: Cf = prod y_k^(e_k-1), value *= Cf,
+// partial k *= Cf, then *= e_k when e_k >= 2.
+template <class R>
+__device__ __forceinline__ void mono_exponents(const DevPlan& P, const Work& W, int q, int m, int vb, long out) {
+  const long S = P.ws_len;
+  auto Y = [&](int k) { return load_c<R>(W.x, P.n, P.mono_var[vb + k]); };
+  auto put = [&](int p, const cplx<R>& v) { store_c<R>(W.ws, S, out + 32L * p, v); };
+  auto get = [&](int p) { return load_c<R>(W.ws, S, out + 32L * p); };
+  cplx<R> cf = c_one<R>();
+  bool have = false;
+  for (int k = 0; k < m; ++k) {
+    const int e = P.mono_exp[vb + k];
+    if (e < 2) continue;
+    const cplx<R> pk = c_powi(Y(k), (unsigned)(e - 1));
+    cf = have ? c_mul(cf, pk) : pk;
+    have = true;
+  }
+  put(0, c_mul(get(0), cf));
+  for (int k = 0; k < m; ++k) {
+    cplx<R> d = c_mul(get(1 + k), cf);
+    const int e = P.mono_exp[vb + k];
+    if (e >= 2) d = c_scale(d, rconst<R>((double)e));
+    put(1 + k, d);
+  }
+}
+
+// Long monomials (size >= kMonoSplit, the first P.mono_long in device order)
+// are evaluated by a PAIR of lanes: the even lane runs the prefix chain
+// F_s = F_{s-1} y_s, the odd lane the suffix chain B_j = y_j B_{j+1}, one
+// multiplication each per step, and each partial d_k = F_{k-1} B_{k+1} is
+// formed by the lane whose operand arrives last, reading the other operand
+// parked (by the partner, at an earlier step or earlier in this step) in the
+// slot of d_k.  Every product has exactly the operands and operand order of
+// the single-thread sweep, so the bits are the same; the dependent chain is
+// m-1 products instead of 2m-4.
+// QD only: a QD multiply is issue bound, so the pair halves the chain; a DD
+// multiply is latency bound and the pair's barriers cost more than they save.
+template <class R>
+constexpr int kMonoSplit = limbs_of<R>::L == 4 ? 8 : (1 << 30);
+
+template <class R>
+__device__ __forceinline__ void mono_pair(const DevPlan& P, const Work& W, int q, bool fwd, unsigned pmask) {
+  const long S = P.ws_len;
+  const int m = P.mono_size[q];
+  const int vb = P.mono_vbeg[q];
+  const long out = P.mono_out[q];
+  auto Y = [&](int k) { return load_c<R>(W.x, P.n, P.mono_var[vb + k]); };
+  auto put = [&](int p, const cplx<R>& v) { store_c<R>(W.ws, S, out + 32L * p, v); };
+  auto get = [&](int p) { return load_c<R>(W.ws, S, out + 32L * p); };
+  // chain values: F_s (fwd lane), B_{m-1-s} (bwd lane).  Both lanes run one
+  // instruction stream (operands chosen by select), so the pair never diverges.
+  cplx<R> c = Y(fwd ? 0 : m - 1);
+  for (int s = 0; s <= m - 2; ++s) {
+    if (s > 0) {
+      const cplx<R> y = Y(fwd ? s : m - 1 - s);
+      c = c_mul(pick(fwd, c, y), pick(fwd, y, c));  // F_{s-1} y_s  |  y_j B_{j+1}
+    }
+    // the partial this chain value feeds: F_s = F_{k-1} with k = s+1;
+    // B_{m-1-s} = B_{k+1} with k = m-2-s.  F ready at step a = k-1, B at b = m-2-k.
+    const int k = fwd ? s + 1 : m - 2 - s;
+    const int a = k - 1, b = m - 2 - k;
+    const bool edge = fwd ? k == m - 1 : k == 0;  // d_{m-1} = F_{m-2}, d_0 = B_1
+    const bool mine_later = fwd ? a > b : a <= b;  // this lane forms d_k in phase 2
+    const int slot = fwd ? (edge ? m : k + 1) : (edge ? 1 : k + 1);
+    if (edge || !mine_later) put(slot, c);  // final partial, or park the operand
+    __syncwarp(pmask);
+    // phase 2: in the first half of the steps neither lane forms a partial
+    // (both park); from the middle on both do (fwd the upper, bwd the lower
+    // half of the partials) -- the same condition in both lanes of the pair
+    if (2 * s >= m - 3) {
+      const bool later = !edge && mine_later;
+      const cplx<R> o = later ? get(k + 1) : c;  // the partner's parked operand
+      const cplx<R> d = c_mul(pick(fwd, c, o), pick(fwd, o, c));  // d_k = F_{k-1} * B_{k+1}
+      if (later) put(k + 1, d);
+    }
+    // no second barrier: phase 2 writes the slot of d_k, which the partner
+    // parked earlier and never touches again
+  }
+  if (fwd) put(0, c_mul(c, Y(m - 1)));  // value = F_{m-2} * y_{m-1}
+  __syncwarp(pmask);
+  if (fwd && (P.mono_flags[q] & 1)) mono_exponents<R>(P, W, q, m, vb, out);
+}
+
 template <class R>
 __device__ __noinline__ void eval_monomials(const DevPlan& P, const Work& W, int tid, int nthreads) {
   const long S = P.ws_len;
-  for (int q = tid; q < P.M; q += nthreads) {
+  {  // long monomials: lane pairs (tid, tid^1) are in the same warp
+    const int pair = tid >> 1, npairs = nthreads >> 1;
+    const unsigned pmask = 3u << (threadIdx.x & 30);
+    for (int q = pair; q < P.mono_long; q += npairs) mono_pair<R>(P, W, q, (tid & 1) == 0, pmask);
+  }
+  for (int q = P.mono_long + tid; q < P.M; q += nthreads) {
     const int m = P.mono_size[q];
     const int vb = P.mono_vbeg[q];
     const long out = P.mono_out[q];
@@ -491,24 +581,7 @@ __device__ __noinline__ void eval_monomials(const DevPlan& P, const Work& W, int
       }
       put(1, B);
     }
-    if (P.mono_flags[q] & 1) {  // exponents >= 2
-      cplx<R> cf = c_one<R>();
-      bool have = false;
-      for (int k = 0; k < m; ++k) {
-        const int e = P.mono_exp[vb + k];
-        if (e < 2) continue;
-        const cplx<R> pk = c_powi(Y(k), (unsigned)(e - 1));
-        cf = have ? c_mul(cf, pk) : pk;
-        have = true;
-      }
-      put(0, c_mul(get(0), cf));
-      for (int k = 0; k < m; ++k) {
-        cplx<R> d = c_mul(get(1 + k), cf);
-        const int e = P.mono_exp[vb + k];
-        if (e >= 2) d = c_scale(d, rconst<R>((double)e));
-        put(1 + k, d);
-      }
-    }
+    if (P.mono_flags[q] & 1) mono_exponents<R>(P, W, q, m, vb, out);
   }
 }
 

@@ -753,6 +753,9 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     dp.n = hp.n;
     dp.N = hp.N;
     dp.M = p->M;
+    dp.mono_long = 0;  // device order is size-descending: count the long ones
+    const int split = prec == PT_QD ? kMonoSplit<qd> : kMonoSplit<dd>;
+    while (dp.mono_long < p->M && hp.mono_size[dp.mono_long] >= split) ++dp.mono_long;
     dp.P_mgs = ptplan::width_mgs(hp.N);
     dp.mgs_gw = ptplan::mgs_group_warps(hp.N);
     dp.mgs_B = warp_mgs_block();
