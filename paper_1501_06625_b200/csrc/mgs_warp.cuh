@@ -279,7 +279,8 @@ struct WarpMgs {
 
   // r_kj = q_k^H a_j, a_j -= r_kj q_k; leaves the updated a_j in a.
   template <int E>
-  __device__ void project(int k, int j, const cplx<R> (&q)[E], cplx<R> (&a)[E], double* col) const {
+  // reg: the column lives in `a` (registers) and is neither loaded nor stored
+  __device__ void project(int k, int j, const cplx<R> (&q)[E], cplx<R> (&a)[E], double* col, bool reg = false) const {
 #ifdef PT_MGS_FINE  // stage clocks of the critical projection (tools/mgs_bench.cu only)
     unsigned long long* fd = (j == k + 1 && lane == 0) ? W.prof + kProfSlots + 6 * (n + 2) + 8 * j : nullptr;
 #define PT_FINE(i, dep) \
@@ -288,7 +289,7 @@ struct WarpMgs {
 #define PT_FINE(i, dep)
 #endif
     PT_FINE(0, q[0].re)
-    load_col(col, N, a);
+    if (!reg) load_col(col, N, a);
     PT_FINE(1, a[0].re)
     cplx<R> v[E];
 #pragma unroll
@@ -296,15 +297,16 @@ struct WarpMgs {
     PT_FINE(2, v[E - 1].im)
     cplx<R> rkj = warp_canon(v, lane, N, kCanonP<E>);
     PT_FINE(3, rkj.re)
-    if (lane == 0) store_c<R>(W.Rm, SR, (long)j * n + k, rkj);
+    const cplx<R> r0 = rkj;
     rkj = shfl0(rkj, 0);
     PT_FINE(4, rkj.im)
     if (j < n || k < n - 1) {
 #pragma unroll
       for (int r = 0; r < E; ++r) a[r] = c_sub(a[r], c_mul(rkj, q[r]));  // rows >= N: ignored garbage
       PT_FINE(5, a[E - 1].im)
-      store_col(col, N, a);
+      if (!reg) store_col(col, N, a);
     }
+    if (lane == 0) store_c<R>(W.Rm, SR, (long)j * n + k, r0);  // off the chain
 #undef PT_FINE
   }
 
@@ -327,8 +329,16 @@ struct WarpMgs {
       }
     }
     if (base > n) return;  // owns no column
-    // stage the owned columns in shared memory (each lane its own rows)
-    for (int j = base, m = 0; j <= n; j += G, ++m) {
+    // The first owned column (slot 0) stays in registers until it is
+    // normalised (its slot then receives q for this CTA's consumers); the
+    // others are staged in shared memory (each lane its own rows).
+    cplx<R> ar[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int i = lane + 32 * r;
+      ar[r] = i < N ? ldcg_c<R>(W.A + (long)base * N, SA, i) : c_zero<R>();
+    }
+    for (int j = base + G, m = 1; j <= n; j += G, ++m) {
       double* col = slot_ptr(m * kWarps + w);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
@@ -339,8 +349,7 @@ struct WarpMgs {
     __syncwarp();
     cplx<R> a[E], q[E];
     if (base == 0) {
-      load_col(slot_ptr(w), N, a);
-      if (!normalize<E, MB>(0, a, slot_ptr(w), 0.0, lane_maxcol) && !MB) return;
+      if (!normalize<E, MB>(0, ar, slot_ptr(w), 0.0, lane_maxcol) && !MB) return;
     }
     const int last = base + ((n - base) / G) * G;
     const long QS = mgs_warp_qs(L, N);
@@ -427,6 +436,17 @@ struct WarpMgs {
       int m = mfirst;
       for (int j = jn; j <= n; j += G, ++m) {
         double* col = slot_ptr(m * kWarps + w);
+        if (m == 0) {  // the register-resident column
+          project(k, j, q, ar, col, true);
+          if (j == k + 1 && j < n) {
+            if (dbg) dbg[3] = clock64() + (unsigned long long)(r_hi(ar[0].re) == 12345.0);
+            if (!normalize<E, MB>(j, ar, col, prev, lane_maxcol, dbg) && !MB) return;
+            if (dbg) dbg[5] = gtimer();
+          } else if (j == n && k == n - 1) {
+            store_col(col, N, ar);  // column n (Q^H b lives in R; keep the slot coherent)
+          }
+          continue;
+        }
         project(k, j, q, a, col);
         if (j == k + 1 && j < n) {
           if (dbg) dbg[3] = clock64() + (unsigned long long)(r_hi(a[0].re) == 12345.0);

@@ -8,11 +8,15 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "../paper_1501_06625_b200/csrc/device.cuh"
 using namespace ptdev;
-using R = dd;
+#ifndef MB_R
+#define MB_R dd
+#endif
+using R = MB_R;
 
 __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* A0, int reps, double* out, int probe) {
   __shared__ Smem<R> sh;
@@ -36,7 +40,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* 
       W.A[q] = A0[q];
     team.sync(&sh.flag);
     if (r == 1) t0 = gtimer();
-    if (probe && team.block == 0 && threadIdx.x >= 192 && threadIdx.x < 224) {
+    if (std::is_same<R, dd>::value && probe && team.block == 0 && threadIdx.x >= 192 && threadIdx.x < 224) {
+#ifndef MB_NO_DD_PROBES
       // concurrent probe: warp 6 of CTA 0 (no columns) runs the isolated
       // projection loop on a private smem slot while the MGS runs
       const int lane = threadIdx.x & 31;
@@ -49,6 +54,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* 
       for (int i = 0; i < 64; ++i) m.template project<2>(3, 10, q, a, scratch);
       long long c1 = clock64();
       if (lane == 0 && r == reps - 1) out[2] = (double)(c1 - c0) / 64 + (a[0].re.hi == 12345.0);
+#endif
     } else
     mgs_warp<R, ClusterTeam>(P, W, team, sh, dyn, 1000ull + r, 0x1p-52);
     team.sync(&sh.flag);
@@ -57,6 +63,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* 
   }
   if (team.block == 0 && threadIdx.x == 0) out[0] = (double)(gtimer() - t0) / max(1, reps - 1);
   // the same projection code in isolation inside this kernel: warp 0 of CTA 0 alone
+#ifndef MB_NO_DD_PROBES
   if (team.block == 0 && threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const WarpMgs<R, ClusterTeam> m{P, W, team, sh, dyn, ColMap{team.nblocks, P.mgs_B}, lane, 0, P.N, P.n, SA,
@@ -68,21 +75,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* 
     long long c1 = clock64();
     if (lane == 0) out[1] = (double)(c1 - c0) / 16 + (a[0].re.hi == 12345.0);
   }
+#endif
 }
 
 int main(int argc, char** argv) {
   const int N = argc > 1 ? atoi(argv[1]) : 64, C = argc > 2 ? atoi(argv[2]) : 16, B = argc > 3 ? atoi(argv[3]) : 4;
   const int reps = argc > 4 ? atoi(argv[4]) : 4;
-  const int n = N, L = 2;
+  const int n = N, L = limbs_of<R>::L;
   const long SA = (long)N * (n + 1);
   std::vector<double> hA(2L * L * SA, 0.0);
   srand(7);
   for (long q = 0; q < SA; ++q) {
     const int i = q % N, j = q / N;
-    hA[q] = (double)rand() / RAND_MAX - 0.5 + (i == j ? 4.0 : 0.0);           // re hi
-    hA[2 * SA + q] = (double)rand() / RAND_MAX - 0.5;                          // im hi
-    hA[SA + q] = hA[q] * 1e-17;                                                // re lo
-    hA[3 * SA + q] = hA[2 * SA + q] * 1e-17;                                   // im lo
+    const double re = (double)rand() / RAND_MAX - 0.5 + (i == j ? 4.0 : 0.0);
+    const double im = (double)rand() / RAND_MAX - 0.5;
+    double sr = re, si = im;
+    for (int l = 0; l < L; ++l) {  // limb l ~ 2^-53 l below the leading one
+      hA[(long)l * SA + q] = sr;
+      hA[(long)(L + l) * SA + q] = si;
+      sr *= 1e-17;
+      si *= 1e-17;
+    }
   }
   DevPlan P{};
   P.n = n;
