@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--prec", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-reference", action="store_true",
+                    help="skip the precision-matched CPU tracker timing (keep the CPU-D comparison)")
     ap.add_argument("--max-steps", type=int, default=None,
                     help="track only a prefix of the path (per-step timing of huge configs)")
     return ap.parse_args()
@@ -187,21 +189,30 @@ def cpu_reference(args, w, seconds):
             "last_steps": stats.steps if stats else None}
 
 
-def cpu_d_all_cores(args):
+def cpu_d_all_cores(args, seconds=2.0):
     """North-star comparison: the reference CPU tracker in complex DOUBLE on
-    all host cores, same system (sec per path)."""
-    from paper_1501_06625_b200 import PrecisionMode, workloads as W
+    all host cores, same system and prefix (--max-steps): seconds per tracked
+    path and per Newton iteration (the per-iteration figure is the fair one
+    for prefixes, whose step counts differ between precisions)."""
+    from paper_1501_06625_b200 import PrecisionMode
     from oracle.orc import Oracle
-    wd = W.chandra(64, PrecisionMode.D) if args.workload == "chandra64" else None
-    if wd is None:
+    a = argparse.Namespace(**vars(args))
+    a.prec = "d"
+    wd = apply_overrides(a, workload(a))
+    if args.workload == "batch32":
         return None
     orc = Oracle("auto")
     orc.set_threads(os.cpu_count() or 1)
-    n, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < 2.0:
-        orc.track_path(0, wd.g, wd.f, wd.gamma, wd.k, wd.start, wd.params)
+    n, iters, t0 = 0, 0, time.perf_counter()
+    while True:
+        _, st, _ = orc.track_path(int(PrecisionMode.D), wd.g, wd.f, wd.gamma, wd.k, wd.start, wd.params)
         n += 1
-    return (time.perf_counter() - t0) / n
+        iters += st.newton_iters
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"sec_per_path": dt / n, "sec_per_newton_iter": dt / max(1, iters), "cores": os.cpu_count() or 1,
+            "paths": n, "newton_iters_per_path": iters / n, "workload": wd.name}
 
 
 def run_reference(args):
@@ -365,10 +376,12 @@ def run_ours(args):
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_reference(args, w, args.cpu_seconds)
+            if not args.no_cpu_reference:
+                line["cpu_baseline"] = cpu_reference(args, w, args.cpu_seconds)
             dall = cpu_d_all_cores(args)
             if dall is not None:
-                line["cpu_d_all_cores_sec_per_path"] = dall
+                line["cpu_d_all_cores"] = dall
+                line["sec_per_newton_iter"] = t_dev_max / args.steps / max(1, stats_list[0].newton_iters)
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
