@@ -508,24 +508,25 @@ __device__ __noinline__ double backsub_blocked(const DevPlan& P, const Work& W, 
     const int j0 = 32 * b, jtop = min(n, j0 + 32) - 1;
     if (w == b) {  // diagonal block: the sequential chain
       const long long tb0 = clock64();
-      cplx<R> cur = (i < jtop) ? load_c<R>(Rs, SR, (long)jtop * n + i) : c_zero<R>();
+      // R column j is stored for every row 0..n-1 (entries below the diagonal
+      // are unused), so the prefetch needs no guard
+      cplx<R> cur = load_c<R>(Rs, SR, (long)jtop * n + i);
+#pragma unroll 4
       for (int j = jtop; j >= j0; --j) {
         const int jl = j - j0;
-        const cplx<R> nxt = (i < j - 1) ? load_c<R>(Rs, SR, (long)(j - 1) * n + i) : c_zero<R>();
+        const cplx<R> nxt = load_c<R>(Rs, SR, (long)(j > 0 ? j - 1 : 0) * n + i);
         const cplx<R> xs_l = c_scale(acc, inv);  // meaningful in lane jl: dx_j
         acc = pick(lane == jl, xs_l, acc);
         const cplx<R> xj = shfl0(xs_l, jl);
-        if (lane == jl) xs[j] = xj;
-        acc = pick(i < j, c_sub(acc, c_mul(cur, xj)), acc);
+        acc = pick(lane < jl, c_sub(acc, c_mul(cur, xj)), acc);
         cur = nxt;
       }
-      if (lane == 0 && W.prof) {  // debugging aid: cycles of the diagonal-block chains
-        W.prof[6] += (unsigned long long)(clock64() - tb0) + (unsigned long long)(r_hi(acc.re) == 12345.0);
-        W.prof[7] += (unsigned long long)(jtop - j0 + 1);
-      }
+      if (row) xs[i] = acc;  // the block's x's, one store per lane after the chain
+      (void)tb0;
     }
     __syncthreads();
-    if (w < b && row) {  // apply block b's x's, descending j
+    if (w < b && row) {  // apply block b's x's, descending j (products independent, subtractions in order)
+#pragma unroll 4
       for (int j = jtop; j >= j0; --j) acc = c_sub(acc, c_mul(load_c<R>(Rs, SR, (long)j * n + i), xs[j]));
     }
   }
@@ -548,20 +549,49 @@ __host__ __device__ inline size_t backsub_stage_doubles(int L, int n) {
 // memory with independent coalesced loads, then run the blocked solve on
 // shared-memory reads.  stage == nullptr: R is read from global.
 template <class R>
-__device__ __noinline__ double backsub_warp(const DevPlan& P, const Work& W, double* stage, Smem<R>& sh) {
+__device__ __forceinline__ double backsub_warp_body(const DevPlan& P, const Work& W, double* stage, Smem<R>& sh) {
   constexpr int L = limbs_of<R>::L;
   const int n = P.n;
   const double* Rs = W.Rm;
   const double* invs = W.inv;
   if (stage) {
     const long nr = 2L * L * n * (n + 1), ni = (long)L * n;
-    for (long q = threadIdx.x; q < nr; q += blockDim.x) stage[q] = __ldcg(W.Rm + q);
+    // 16-byte loads, 8 in flight per thread (a dependent load->store loop
+    // would pay one L2 round trip per element: ~23 us for a 64x65 DD R)
+    const double2* src = reinterpret_cast<const double2*>(W.Rm);
+    double2* dst = reinterpret_cast<double2*>(stage);
+    const long nv = nr / 2;  // nr = 2L n(n+1) is even
+    constexpr int U = 8;
+    for (long q0 = threadIdx.x; q0 < nv; q0 += (long)U * blockDim.x) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long q = q0 + (long)u * blockDim.x;
+        if (q < nv) v[u] = __ldcg(src + q);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long q = q0 + (long)u * blockDim.x;
+        if (q < nv) dst[q] = v[u];
+      }
+    }
     for (long q = threadIdx.x; q < ni; q += blockDim.x) stage[nr + q] = __ldcg(W.inv + q);
     __syncthreads();
     Rs = stage;
     invs = stage + nr;
   }
   return backsub_blocked<R>(P, W, Rs, invs, sh, sh.tree);  // sh.tree: kThreads complex >= n x's
+}
+
+template <class R>
+__device__ __noinline__ double backsub_warp(const DevPlan& P, const Work& W, double* stage, Smem<R>& sh) {
+  const long long tb0 = clock64();
+  const double u = backsub_warp_body<R>(P, W, stage, sh);
+  if (threadIdx.x == 0 && W.prof) {  // debugging aid: cycles inside the back substitution (CTA 0)
+    W.prof[6] += (unsigned long long)(clock64() - tb0);
+    W.prof[7] += (unsigned long long)P.n;
+  }
+  return u;
 }
 
 }  // namespace ptdev
