@@ -563,7 +563,7 @@ int setup_cluster(pt_plan* p) {
   p->cluster_size = 0;
   const char* ce = getenv("PT_CLUSTER_MAX");  // tuning knob: cap the cluster size
   const int cmax = ce ? atoi(ce) : 16;
-  for (int c : {16, 8, 4, 2}) {
+  for (int c : {16, 8, 4, 2, 1}) {
     if (c > cmax) continue;
     int warp = 0;
     const size_t dyn = engine_smem(p->L, p->N, p->n, c, true, &warp);
@@ -593,6 +593,8 @@ int setup_cluster(pt_plan* p) {
   // small enough that 16 SMs do not starve it run on the cluster engine
   const double contributions = (double)p->n_ctr;
   p->engine = (p->cluster_size >= 8 && p->n <= 192 && contributions <= 2e5) ? 1 : 0;
+  const char* ee = getenv("PT_ENGINE");  // tuning knob: 0 grid, 1 cluster
+  if (ee && (ee[0] == '0' || (ee[0] == '1' && p->cluster_size > 0))) p->engine = ee[0] - '0';
   return PT_OK;
 }
 
