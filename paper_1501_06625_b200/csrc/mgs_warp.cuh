@@ -28,7 +28,11 @@
 
 namespace ptdev {
 
-constexpr int kWarpMgsMaxN = 128;  // E <= 4 elements per lane, width_mgs(N) <= 64
+constexpr int kWarpMgsMaxN = 128;
+
+#ifndef PT_MGS_WARP_INLINE
+#define PT_MGS_WARP_INLINE __noinline__
+#endif  // E <= 4 elements per lane, width_mgs(N) <= 64
 
 struct ColMap {
   int C, B;  // CTAs in the team, columns per CTA block
@@ -461,7 +465,7 @@ struct WarpMgs {
 // one register-allocation unit per E (a QD E = 4 body must not make the
 // E = 2 body spill)
 template <class R, class Team, int E>
-__device__ __noinline__ void mgs_warp_e(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
+__device__ PT_MGS_WARP_INLINE void mgs_warp_e(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                                         unsigned long long epoch, double sqrt_eps) {
   constexpr int L = limbs_of<R>::L;
   double* qb = colsm + mgs_warp_slots_doubles(L, P.N, P.n, team.nblocks);

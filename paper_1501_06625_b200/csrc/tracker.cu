@@ -74,7 +74,7 @@ Layout make_layout(int L, int n, int N, long ws_len) {
   o.ctl = u;
   u += 32;
   o.prof = u;
-  u += kProfSlots + 6 * (n + 2) + 32;
+  u += kProfSlots + 14 * (n + 2) + 32;  // + per-column fine markers (PT_MGS_FINE builds)
   o.uslice = u;
   return o;
 }
@@ -959,7 +959,7 @@ int pt_plan_mgs_timeline(pt_plan* p, double* out, int32_t count) {
   if (!p || !out) return PT_E_INVAL;
   PT_CUDA(cudaSetDevice(p->device));
   PT_CUDA(cudaStreamSynchronize(p->stream));
-  const int m = std::min(count, 6 * (p->n + 1));
+  const int m = std::min(count, 14 * (p->n + 2));
   std::vector<unsigned long long> h(m);
   PT_CUDA(cudaMemcpy(h.data(), carve(p->dwork, p->uwork, p->lay, 0).prof + kProfSlots, m * 8, cudaMemcpyDeviceToHost));
   for (int i = 0; i < m; ++i) out[i] = (double)h[i];

@@ -31,5 +31,13 @@ out = {"workload": w.name, "engine": hom.engine, "per_column_median": {
     "column_ns (q_{j-1} pushed -> q_j pushed)": med([t[j, 5] - t[j - 1, 5] for j in cols])},
     "total_ns": float(t[n - 1, 5] - t[1, 0])}
 print(json.dumps(out))
+if os.environ.get("MGS_FINE"):  # library built with -DPT_MGS_FINE
+    f = np.zeros(14 * (n + 2))
+    # pt_plan_mgs_timeline returns prof[kProfSlots:...]; fine markers follow the 6 (n+2) timeline words
+    big = np.zeros(6 * (n + 2) + 8 * (n + 2))
+    nat.check(nat.lib.pt_plan_mgs_timeline(hom.plan, nat.dptr(big), big.size))
+    fm = big[6 * (n + 2):].reshape(n + 2, 8)
+    names = ["load_col", "conj_mul", "tree", "bcast", "axpy"]
+    print(json.dumps({"fine_cycles_median": {names[q]: float(np.median([fm[j, q + 1] - fm[j, q] for j in cols])) for q in range(5)}}))
 if os.environ.get("MGS_DUMP"):
     print(" ".join(f"{j}:{int(t[j, 3] - t[j, 2])}/{int(t[j, 4] - t[j, 3])}" for j in cols))
