@@ -24,6 +24,6 @@ from .tracker import (  # noqa: F401
     total_degree_start,
     unit_complex,
 )
-from . import workloads  # noqa: F401
+from . import monodromy, workloads  # noqa: F401
 
 __version__ = "0.1.0"
