@@ -219,15 +219,16 @@ struct WarpMgs {
     const unsigned need = __ballot_sync(0xffffffffu, lane < team.nblocks && lane_maxcol > j);
     const unsigned remote = need & ~(1u << team.block);
     double* msg = W.qg + (long)j * QS;
+    // this CTA's consumers read the owner's slot (stored by the caller): release
+    // them first -- the global staging and its proxy fence are for remote CTAs only
+    __syncwarp();
+    if (lane == 0 && ((need >> team.block) & 1u)) mbar_arrive_local(bars() + j);
     if (remote) {
       store_col(msg, N, a);
       if (lane == 0) msg[2 * L * N] = pmax;
       asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> async-proxy (TMA) reads
-    }
-    __syncwarp();
-    if (lane == 0) {
-      if ((need >> team.block) & 1u) mbar_arrive_local(bars() + j);
-      if (remote) bulk_multicast(qbuf() + (long)j * QS, msg, (uint32_t)(QS * 8), bars() + j, (uint16_t)remote);
+      __syncwarp();
+      if (lane == 0) bulk_multicast(qbuf() + (long)j * QS, msg, (uint32_t)(QS * 8), bars() + j, (uint16_t)remote);
     }
   }
 
