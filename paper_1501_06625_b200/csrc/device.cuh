@@ -661,47 +661,25 @@ __device__ __forceinline__ cplx<R> lane_sum(const DevPlan& P, const Work& W, int
 
 template <class R>
 __device__ __forceinline__ cplx<R> lane_canon32(const DevPlan& P, const Work& W, int beg, int K) {
-  // Leaves are processed 8 at a time: their index loads, then their value
-  // loads and first two contributions are issued unconditionally (clamped
-  // indices; empty leaves are computed and discarded), so a lane keeps 8-16
-  // independent L2 round trips in flight instead of one per contribution.
-  constexpr int kG = limbs_of<R>::L == 4 ? 4 : 8;
   cplx<R> st[6];
   bool ne[6];
 #pragma unroll
-  for (int t0 = 0; t0 < 32; t0 += kG) {
-    int ci[kG], wi[kG], ci2[kG], wi2[kG];
-#pragma unroll
-    for (int u = 0; u < kG; ++u) {
-      const int p = brev5(t0 + u);
-      const bool h1 = p < K, h2 = p + 32 < K;
-      ci[u] = h1 ? P.ctr_coef[beg + p] : 0;
-      wi[u] = h1 ? P.ctr_ws[beg + p] : -1;
-      ci2[u] = h2 ? P.ctr_coef[beg + p + 32] : 0;
-      wi2[u] = h2 ? P.ctr_ws[beg + p + 32] : -1;
+  for (int t = 0; t < 32; ++t) {
+    const int p = brev5(t);
+    const int d = popc5(t);  // stack depth before this leaf
+    cplx<R> v = c_zero<R>();
+    const bool has = p < K;
+    if (has) {
+      v = contrib<R>(P, W, P.ctr_coef[beg + p], P.ctr_ws[beg + p]);
+      for (int r = p + 32; r < K; r += 32) v = c_add(v, contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]));
     }
-    cplx<R> v[kG];
+    st[d] = v;
+    ne[d] = has;
+    // merges after leaf t: as many as trailing zeros of t + 1
 #pragma unroll
-    for (int u = 0; u < kG; ++u) {
-      const int p = brev5(t0 + u);
-      v[u] = contrib<R>(P, W, ci[u], wi[u]);
-      if (p + 32 < K) {
-        v[u] = c_add(v[u], contrib<R>(P, W, ci2[u], wi2[u]));
-        for (int r = p + 64; r < K; r += 32) v[u] = c_add(v[u], contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kG; ++u) {
-      const int t = t0 + u;
-      const int d = popc5(t);  // stack depth before this leaf
-      st[d] = v[u];
-      ne[d] = brev5(t) < K;
-      // merges after leaf t: as many as trailing zeros of t + 1
-#pragma unroll
-      for (int m = 0; m < ctz6(t + 1); ++m) {
-        const int top = d - m;
-        if (ne[top]) st[top - 1] = c_add(st[top - 1], st[top]);
-      }
+    for (int m = 0; m < ctz6(t + 1); ++m) {
+      const int top = d - m;
+      if (ne[top]) st[top - 1] = c_add(st[top - 1], st[top]);
     }
   }
   return st[0];

@@ -26,6 +26,8 @@
 // columns base(c, w) + m G, m = 0, 1, ...  (slot m of its smem column area).
 #pragma once
 
+#include <type_traits>
+
 namespace ptdev {
 
 constexpr int kWarpMgsMaxN = 128;
@@ -158,11 +160,14 @@ template <class R, class Team>
 struct WarpMgs {
   static constexpr int L = limbs_of<R>::L;
   const DevPlan& P;
-  // Work and Team by value: through references every store to shared or
-  // global memory may alias them, so their pointers would be reloaded (from
-  // the kernel's stack) on the critical chain after each store.
-  const Work W;
-  const Team team;
+  // Work and Team by value in the single-path engines: through references
+  // every store to shared or global memory may alias them, so their pointers
+  // would be reloaded (from the kernel's stack) on the critical chain after
+  // each store.  The batch kernel (BlockTeam, 128 registers per thread) keeps
+  // references: there the extra ~30 registers cost more in spills.
+  static constexpr bool kByValue = !std::is_same<Team, BlockTeam>::value;
+  std::conditional_t<kByValue, const Work, const Work&> W;
+  std::conditional_t<kByValue, const Team, const Team&> team;
   Smem<R>& sh;
   double* colsm;  // this CTA's dynamic smem (layout above)
   ColMap cm;

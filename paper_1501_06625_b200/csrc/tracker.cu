@@ -151,8 +151,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Batch CTAs per SM: two paths share an SM in D / DD (128 registers per
 // thread suffice there); QD keeps the whole register file for one path.
+#ifndef PT_BATCH_CTAS
+#define PT_BATCH_CTAS 2
+#endif
 template <class R>
-constexpr int kBatchCtasPerSm = limbs_of<R>::L == 4 ? 1 : 2;
+constexpr int kBatchCtasPerSm = limbs_of<R>::L == 4 ? 1 : PT_BATCH_CTAS;
 
 template <class R>
 __global__ void __launch_bounds__(kThreads, kBatchCtasPerSm<R>)

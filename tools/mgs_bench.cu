@@ -97,6 +97,14 @@ int main(int argc, char** argv) {
       si *= 1e-17;
     }
   }
+  if (const char* fn = getenv("MGS_MATRIX")) {  // [2L][N*(n+1)] doubles (SoA planes), e.g. chandra's [J | -h]
+    FILE* fp = fopen(fn, "rb");
+    if (fp) {
+      const size_t got = fread(hA.data(), 8, hA.size(), fp);
+      fclose(fp);
+      printf("{\"matrix\": \"%s\", \"doubles\": %zu}\n", fn, got);
+    }
+  }
   DevPlan P{};
   P.n = n;
   P.N = N;
