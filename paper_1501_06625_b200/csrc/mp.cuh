@@ -381,11 +381,14 @@ PT_HDI qd qd_renorm5(double c0, double c1, double c2, double c3, double c4) {
 //   3 the same network comparing magnitudes as integers on the FP64 bits;
 //   2 insertion position by mask; 1 plain insertion; 0 insertion with a
 //     warp-uniform early exit (integer keys).
+#ifndef PT_QD_MUL_LEVELS
+#define PT_QD_MUL_LEVELS 1
+#endif
 #ifndef PT_QD_SORT
 #define PT_QD_SORT 4
 #endif
 template <int K>
-PT_HD qd qd_distill(double (&m)[K]) {
+PT_HD void qd_sort(double (&m)[K]) {
 #if PT_QD_SORT == 2
   // Insertion position by mask: all compares of the sorted prefix against v
   // are independent; pos = 1 + index of the highest prefix entry with
@@ -456,6 +459,11 @@ PT_HD qd qd_distill(double (&m)[K]) {
     if (moving) m[0] = v;
   }
 #endif
+}
+
+// qd_distill after the sort: two two_sum sweeps, tail, renorm5 (multiprec.hpp:269-278)
+template <int K>
+PT_HD qd qd_distill_sorted(double (&m)[K]) {
   if (!finite(m[0])) return {{m[0], 0.0, 0.0, 0.0}};
 #pragma unroll
   for (int pass = 0; pass < 2; ++pass) {
@@ -470,6 +478,27 @@ PT_HD qd qd_distill(double (&m)[K]) {
   const double c2 = K > 2 ? m[K > 2 ? 2 : 0] : 0.0;
   const double c3 = K > 3 ? m[K > 3 ? 3 : 0] : 0.0;
   return qd_renorm5(c0, c1, c2, c3, tail);
+}
+
+template <int K>
+PT_HD qd qd_distill(double (&m)[K]) {
+  qd_sort<K>(m);
+  return qd_distill_sorted<K>(m);
+}
+
+// Stable odd-even transposition on G values (descending |.|, strict swaps).
+template <int G>
+PT_HD void oe_sort(double (&g)[G]) {
+#pragma unroll
+  for (int r = 0; r < G; ++r) {
+#pragma unroll
+    for (int i = r & 1; i + 1 < G; i += 2) {
+      const double a = g[i], b = g[i + 1];
+      const bool sw = fabs_cmp_lt(a, b);
+      g[i] = sw ? b : a;
+      g[i + 1] = sw ? a : b;
+    }
+  }
 }
 
 PT_HD qd r_from(double x, qd*) { return {{x, 0.0, 0.0, 0.0}}; }
@@ -494,6 +523,34 @@ PT_QDOP qd r_mul(qd a, qd b) {  // multiprec.hpp:297-312
   m[20] = mul64(a.c[1], b.c[3]);
   m[21] = mul64(a.c[2], b.c[2]);
   m[22] = mul64(a.c[3], b.c[1]);
+#if PT_QD_MUL_LEVELS
+  // Fast path, same permutation: group the 23 addends by "level" i+j of
+  // p_ij = fl(a_i b_j) (level i+j+1 for its error e_ij and for the three
+  // plain products), each group listed in input order:
+  //   G0 {p00}  G1 {e00 p01 p10}  G2 {e01 p02 e10 p11 p20}
+  //   G3 {e02 p03 e11 p12 e20 p21 p30}  G4 {e03 e12 e21 e30 x13 x22 x31}.
+  // Sort each group stably (55 compare-exchanges instead of 253).  If every
+  // element of each group is STRICTLY larger in magnitude than every element
+  // of the next (4 checks on the sorted groups' ends), the concatenation is
+  // the stable sort of all 23 -- exactly the reference's insertion-sort
+  // permutation.  Otherwise (zeros, short or non-canonical operands, NaN)
+  // the full network sorts the original array.
+  double g1[3] = {m[1], m[2], m[8]};
+  double g2[5] = {m[3], m[4], m[9], m[10], m[14]};
+  double g3[7] = {m[5], m[6], m[11], m[12], m[15], m[16], m[18]};
+  double g4[7] = {m[7], m[13], m[17], m[19], m[20], m[21], m[22]};
+  oe_sort<3>(g1);
+  oe_sort<5>(g2);
+  oe_sort<7>(g3);
+  oe_sort<7>(g4);
+  const bool levels = fabs_cmp_lt(g1[0], m[0]) && fabs_cmp_lt(g2[0], g1[2]) && fabs_cmp_lt(g3[0], g2[4]) &&
+                      fabs_cmp_lt(g4[0], g3[6]);
+  if (levels) {
+    double s[23] = {m[0],  g1[0], g1[1], g1[2], g2[0], g2[1], g2[2], g2[3], g2[4], g3[0], g3[1], g3[2],
+                    g3[3], g3[4], g3[5], g3[6], g4[0], g4[1], g4[2], g4[3], g4[4], g4[5], g4[6]};
+    return qd_distill_sorted<23>(s);
+  }
+#endif
   return qd_distill<23>(m);
 }
 PT_QDOP qd r_mul_d(qd a, double b) {  // multiprec.hpp:314-323
