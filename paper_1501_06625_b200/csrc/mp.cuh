@@ -524,6 +524,18 @@ PT_QDOP qd r_mul(qd a, qd b) {  // multiprec.hpp:297-312
   m[21] = mul64(a.c[2], b.c[2]);
   m[22] = mul64(a.c[3], b.c[1]);
 #if PT_QD_MUL_LEVELS
+  // Short left operand (a = (a0, 0, 0, 0): coefficients built from doubles,
+  // Rng::box / complex_from): every addend with index >= 8 is a product with
+  // a zero limb, i.e. +-0, and all indices >= 8 follow 0..7.  The stable sort
+  // is then the stable sort of m[0..7] (its zeros sink to its end in index
+  // order) followed by m[8..22] unchanged.
+  if (a.c[1] == 0.0 && a.c[2] == 0.0 && a.c[3] == 0.0) {
+    double s8[8] = {m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7]};
+    oe_sort<8>(s8);
+    double s[23] = {s8[0], s8[1], s8[2],  s8[3],  s8[4],  s8[5],  s8[6],  s8[7],  m[8],  m[9],  m[10], m[11],
+                    m[12], m[13], m[14], m[15], m[16], m[17], m[18], m[19], m[20], m[21], m[22]};
+    return qd_distill_sorted<23>(s);
+  }
   // Fast path, same permutation: group the 23 addends by "level" i+j of
   // p_ij = fl(a_i b_j) (level i+j+1 for its error e_ij and for the three
   // plain products), each group listed in input order:
