@@ -64,6 +64,7 @@ struct DevPlan {
   int mgs_warp;  // 1: warp-per-column MGS + one-warp back substitution (mgs_warp.cuh, N <= 128)
   int mgs_B;     // warp MGS: consecutive columns per CTA block (divides kWarps)
   int bs_smem;   // warp back substitution stages R in CTA 0's dynamic shared memory
+  int x_smem;    // monomial evaluation reads x from a per-CTA shared-memory copy
 };
 
 // One path's workspace.  All arrays are complex SoA unless noted.
@@ -463,9 +464,10 @@ __device__ void weights(const DevPlan& P, double t, cplx<R>& wS, R& wT) {
 // Exponents >= 2: Cf = prod y_k^(e_k-1), value *= Cf,
 // partial k *= Cf, then *= e_k when e_k >= 2.
 template <class R>
-__device__ __forceinline__ void mono_exponents(const DevPlan& P, const Work& W, int q, int m, int vb, long out) {
+__device__ __forceinline__ void mono_exponents(const DevPlan& P, const Work& W, const double* xs, int q, int m, int vb,
+                                               long out) {
   const long S = P.ws_len;
-  auto Y = [&](int k) { return load_c<R>(W.x, P.n, P.mono_var[vb + k]); };
+  auto Y = [&](int k) { return load_c<R>(xs, P.n, P.mono_var[vb + k]); };
   auto put = [&](int p, const cplx<R>& v) { store_c<R>(W.ws, S, out + 32L * p, v); };
   auto get = [&](int p) { return load_c<R>(W.ws, S, out + 32L * p); };
   cplx<R> cf = c_one<R>();
@@ -501,12 +503,13 @@ template <class R>
 constexpr int kMonoSplit = limbs_of<R>::L == 4 ? 8 : (1 << 30);
 
 template <class R>
-__device__ __forceinline__ void mono_pair(const DevPlan& P, const Work& W, int q, bool fwd, unsigned pmask) {
+__device__ __forceinline__ void mono_pair(const DevPlan& P, const Work& W, const double* xs, int q, bool fwd,
+                                          unsigned pmask) {
   const long S = P.ws_len;
   const int m = P.mono_size[q];
   const int vb = P.mono_vbeg[q];
   const long out = P.mono_out[q];
-  auto Y = [&](int k) { return load_c<R>(W.x, P.n, P.mono_var[vb + k]); };
+  auto Y = [&](int k) { return load_c<R>(xs, P.n, P.mono_var[vb + k]); };
   auto put = [&](int p, const cplx<R>& v) { store_c<R>(W.ws, S, out + 32L * p, v); };
   auto get = [&](int p) { return load_c<R>(W.ws, S, out + 32L * p); };
   // chain values: F_s (fwd lane), B_{m-1-s} (bwd lane).  Both lanes run one
@@ -540,22 +543,26 @@ __device__ __forceinline__ void mono_pair(const DevPlan& P, const Work& W, int q
   }
   if (fwd) put(0, c_mul(c, Y(m - 1)));  // value = F_{m-2} * y_{m-1}
   __syncwarp(pmask);
-  if (fwd && (P.mono_flags[q] & 1)) mono_exponents<R>(P, W, q, m, vb, out);
+  if (fwd && (P.mono_flags[q] & 1)) mono_exponents<R>(P, W, xs, q, m, vb, out);
 }
 
+// xs: x (2L planes of n) -- a per-CTA shared-memory copy when P.x_smem, else W.x.
+// The single-thread sweeps prefetch the next factor (and, backwards, the
+// parked prefix product) one step ahead, so the chain of products does not
+// wait on an index load and a value load per step.
 template <class R>
-__device__ __noinline__ void eval_monomials(const DevPlan& P, const Work& W, int tid, int nthreads) {
+__device__ __noinline__ void eval_monomials(const DevPlan& P, const Work& W, const double* xs, int tid, int nthreads) {
   const long S = P.ws_len;
   {  // long monomials: lane pairs (tid, tid^1) are in the same warp
     const int pair = tid >> 1, npairs = nthreads >> 1;
     const unsigned pmask = 3u << (threadIdx.x & 30);
-    for (int q = pair; q < P.mono_long; q += npairs) mono_pair<R>(P, W, q, (tid & 1) == 0, pmask);
+    for (int q = pair; q < P.mono_long; q += npairs) mono_pair<R>(P, W, xs, q, (tid & 1) == 0, pmask);
   }
   for (int q = P.mono_long + tid; q < P.M; q += nthreads) {
     const int m = P.mono_size[q];
     const int vb = P.mono_vbeg[q];
     const long out = P.mono_out[q];
-    auto Y = [&](int k) { return load_c<R>(W.x, P.n, P.mono_var[vb + k]); };
+    auto Y = [&](int k) { return load_c<R>(xs, P.n, P.mono_var[vb + k]); };
     auto put = [&](int p, const cplx<R>& v) { store_c<R>(W.ws, S, out + 32L * p, v); };
     auto get = [&](int p) { return load_c<R>(W.ws, S, out + 32L * p); };
     if (m == 1) {
@@ -569,19 +576,28 @@ __device__ __noinline__ void eval_monomials(const DevPlan& P, const Work& W, int
     } else {
       cplx<R> F = Y(0);
       put(2, F);
+      cplx<R> yn = Y(1);
       for (int k = 1; k <= m - 2; ++k) {
-        F = c_mul(F, Y(k));
+        const cplx<R> y = yn;
+        yn = Y(k + 1);  // k + 1 <= m - 1: the last one is y_{m-1}
+        F = c_mul(F, y);
         put(k + 2, F);
       }
-      put(0, c_mul(F, Y(m - 1)));
-      cplx<R> B = Y(m - 1);
+      put(0, c_mul(F, yn));
+      cplx<R> B = yn;  // y_{m-1}
+      cplx<R> yk = Y(m - 2), fk = get(m - 1);
       for (int k = m - 2; k >= 1; --k) {
-        put(k + 1, c_mul(get(k + 1), B));
-        B = c_mul(Y(k), B);
+        const cplx<R> y = yk, f = fk;
+        if (k > 1) {
+          yk = Y(k - 1);
+          fk = get(k);
+        }
+        put(k + 1, c_mul(f, B));
+        B = c_mul(y, B);
       }
       put(1, B);
     }
-    if (P.mono_flags[q] & 1) mono_exponents<R>(P, W, q, m, vb, out);
+    if (P.mono_flags[q] & 1) mono_exponents<R>(P, W, xs, q, m, vb, out);
   }
 }
 
@@ -1229,7 +1245,14 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
   for (int it = 1; it <= sp.newton_max_iter; ++it) {
     o.iters = it;
     if (pc.on) W.prof[PROF_ITERS] += 1;
-    eval_monomials<R>(P, W, tid, nth);
+    const double* xs = W.x;
+    if (P.x_smem) {  // every CTA stages x in its dynamic shared memory (free during evaluation)
+      constexpr int L = limbs_of<R>::L;
+      for (int i = threadIdx.x; i < 2 * L * P.n; i += kThreads) colsm[i] = W.x[i];
+      __syncthreads();
+      xs = colsm;
+    }
+    eval_monomials<R>(P, W, xs, tid, nth);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     pc.lap(W.prof + PROF_MONO);
     eval_slots<R, Team>(P, W, team, sh, t);

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (team.block == 0)
     for (int i = threadIdx.x; i < n; i += kThreads) store_c<R>(W.x, n, i, load_c<R>(x, n, i));
   if (!team.sync(&sh.flag)) return;
-  eval_monomials<R>(P, W, team.block * kThreads + threadIdx.x, team.nblocks * kThreads);
+  eval_monomials<R>(P, W, W.x, team.block * kThreads + threadIdx.x, team.nblocks * kThreads);
   if (!team.sync(&sh.flag)) return;
   eval_slots<R, GridTeam>(P, W, team, sh, t);
   if (!team.sync(&sh.flag)) return;
@@ -625,6 +625,8 @@ int guarded(F&& f) {
 int stage_fits(const pt_plan* p, size_t dyn_bytes) {
   return backsub_stage_doubles(p->L, p->n) * 8 <= dyn_bytes ? 1 : 0;
 }
+// the monomial evaluation can read x from a shared-memory copy
+int x_fits(const pt_plan* p, size_t dyn_bytes) { return (size_t)2 * p->L * p->n * 8 <= dyn_bytes ? 1 : 0; }
 
 template <class R>
 void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
@@ -635,6 +637,7 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
     dp.mgs_smem = p->cluster_dyn_smem > 0;
     dp.mgs_warp = p->cluster_warp;
     dp.bs_smem = stage_fits(p, p->cluster_dyn_smem);
+    dp.x_smem = x_fits(p, p->cluster_dyn_smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p->cluster_size);
     cfg.blockDim = dim3(kThreads);
@@ -654,6 +657,7 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
   dp.mgs_smem = p->grid_dyn_smem > 0;
   dp.mgs_warp = p->grid_warp;
   dp.bs_smem = stage_fits(p, p->grid_dyn_smem);
+  dp.x_smem = x_fits(p, p->grid_dyn_smem);
   pt_step_params spc = sp;
   TrackIO ioc = io;
   void* args[] = {&dp, &W, &spc, &ioc, &epoch};
@@ -1068,6 +1072,7 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   bdp.mgs_smem = p->batch_dyn_smem > 0;
   bdp.mgs_warp = p->batch_warp;
   bdp.bs_smem = stage_fits(p, p->batch_dyn_smem);
+  bdp.x_smem = x_fits(p, p->batch_dyn_smem);
   bdp.tasks = p->tasks_b;
   for (int c = 0; c < 6; ++c) bdp.class_beg[c] = p->class_beg_b[c];
   // launched as clusters of one CTA: the warp MGS pushes q_k with st.async,
