@@ -573,6 +573,29 @@ PT_QDOP qd r_mul_d(qd a, double b) {  // multiprec.hpp:314-323
     m[2 * i] = two_prod(a.c[i], b, e);
     m[2 * i + 1] = e;
   }
+#if PT_QD_MUL_LEVELS
+  // Same permutation, cheaper (cf. r_mul): addends m = p0 e0 p1 e1 p2 e2 p3 e3.
+  //  * exact products (all e_i == 0, e.g. b = 0.5) with |p0|>|p1|>|p2|>|p3|>0:
+  //    the stable sort is p0 p1 p2 p3 then the four zeros in index order;
+  //  * else level groups {p0} {e0 p1} {e1 p2} {e2 p3} {e3}, each sorted stably,
+  //    valid when every group is strictly larger than the next.
+  if (m[1] == 0.0 && m[3] == 0.0 && m[5] == 0.0 && m[7] == 0.0 && fabs_cmp_lt(m[2], m[0]) &&
+      fabs_cmp_lt(m[4], m[2]) && fabs_cmp_lt(m[6], m[4]) && m[6] != 0.0) {
+    double s[8] = {m[0], m[2], m[4], m[6], m[1], m[3], m[5], m[7]};
+    return qd_distill_sorted<8>(s);
+  }
+  {
+    double g1[2] = {m[1], m[2]}, g2[2] = {m[3], m[4]}, g3[2] = {m[5], m[6]};
+    oe_sort<2>(g1);
+    oe_sort<2>(g2);
+    oe_sort<2>(g3);
+    if (fabs_cmp_lt(g1[0], m[0]) && fabs_cmp_lt(g2[0], g1[1]) && fabs_cmp_lt(g3[0], g2[1]) &&
+        fabs_cmp_lt(m[7], g3[1])) {
+      double s[8] = {m[0], g1[0], g1[1], g2[0], g2[1], g3[0], g3[1], m[7]};
+      return qd_distill_sorted<8>(s);
+    }
+  }
+#endif
   return qd_distill<8>(m);
 }
 PT_QDOP qd r_div(qd a, qd b) {  // multiprec.hpp:327-337
