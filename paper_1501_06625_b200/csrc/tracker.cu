@@ -623,6 +623,8 @@ int guarded(F&& f) {
 
 // the warp back substitution can stage R in the engine's dynamic smem
 int stage_fits(const pt_plan* p, size_t dyn_bytes) {
+  const char* e = getenv("PT_BS_SMEM");  // tuning knob: 0 reads R from L2 in the back substitution
+  if (e && e[0] == '0') return 0;
   return backsub_stage_doubles(p->L, p->n) * 8 <= dyn_bytes ? 1 : 0;
 }
 // the monomial evaluation can read x from a shared-memory copy
