@@ -117,3 +117,22 @@ def test_track_batch_bitwise(gpu, oracle):
         assert (outs[p].steps, outs[p].newton_iters, outs[p].success) == (st_ref.steps, st_ref.newton_iters,
                                                                          st_ref.status == 0)
         assert_bits_equal(ends[p], end_ref, f"path {p}")
+
+
+# Mid-size systems: the warp MGS with E = 3..4 rows per lane (width_mgs = 64,
+# lane-local off = 32 level), both hand-off variants (TMA multicast when the
+# Q buffer fits in shared memory, DSMEM + flags otherwise), and the canonical
+# trees with partial (N < 32 E) and full (N = 32 E) warps.  Short prefixes
+# keep the CPU oracle fast; every trial, the stats and the end point must be
+# bit-identical, whatever the path does.
+@pytest.mark.parametrize("engine", ["grid", "cluster"])
+@pytest.mark.parametrize("n,prec", [(80, PM.D), (80, PM.DD), (128, PM.DD), (72, PM.QD)])
+def test_track_midsize_bitwise(gpu, oracle, n, prec, engine):
+    w = W.random_system(n=n, degree=2, n_monomials=24, prec=prec, seed=n)
+    w.params.max_steps = 3
+    cap = w.params.max_steps + 2
+    end_ref, st_ref, tr_ref = oracle.track_path(int(prec), w.g, w.f, w.gamma, w.k, w.start, w.params, cap)
+    hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)
+    hom.set_engine(engine)
+    out = hom.track_path(w.start, w.params, trace=True)
+    _compare_track(w, out, end_ref, st_ref, tr_ref)
