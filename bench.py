@@ -163,6 +163,29 @@ def path_work(hom, stats_list, degree):
     return total, we, ws
 
 
+def critical_path(hom, st, prof, steps):
+    """Latency view of a single path (the FP64-pipe fraction is tiny by
+    construction): the MGS sweep is a chain of n dependent column steps
+    (project column k+1 with q_k, normalise it, hand q_{k+1} on).  From the
+    device timeline of the last sweep: median ns per column step, and the
+    share of the measured MGS time that n x solves x that step explains."""
+    from paper_1501_06625_b200 import _native as nat
+    n = hom.n
+    buf = np.zeros(6 * (n + 1))
+    if nat.lib.pt_plan_mgs_timeline(hom.plan, nat.dptr(buf), buf.size) != 0:
+        return None
+    t = buf.reshape(n + 1, 6)
+    cols = [j for j in range(2, n) if t[j, 5] > 0 and t[j - 1, 5] > 0]
+    if not cols:
+        return None
+    col_ns = float(np.median([t[j, 5] - t[j - 1, 5] for j in cols]))
+    mgs_ns = prof[2] / steps
+    chain_ns = col_ns * n * st.solves
+    return {"columns_per_solve": n, "solves": int(st.solves), "ns_per_column_step": col_ns,
+            "chain_share_of_mgs": chain_ns / mgs_ns if mgs_ns > 0 else None,
+            "mgs_share_of_phases": float(prof[2] / sum(prof[:5])) if sum(prof[:5]) > 0 else None}
+
+
 def cpu_reference(args, w, seconds):
     """The reference CPU tracker on this host's cores: oracle/_ref (SPEC
     tracker on the unmodified reference headers), else the oracle port."""
@@ -373,6 +396,7 @@ def run_ours(args):
                 k: prof[i] * 1e-6 / args.steps for i, k in enumerate(
                     ["monomials", "slot_sums", "mgs", "backsub_update", "predict"])},
             "newton_iters_timed": None if batch else prof[5] / args.steps,
+            "critical_path": None if batch else critical_path(hom, stats_list[0], prof, args.steps),
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
