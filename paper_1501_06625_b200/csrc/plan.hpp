@@ -17,6 +17,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -62,7 +63,11 @@ struct SlotTask {
 // throughput bound and runs everything up to 128 contributions on lanes, so
 // no lane idles through a warp tree of a short sum.
 inline int lane_k(int L) { return L == 4 ? 4 : 8; }
-inline int lane_k_batch(int L) { return L == 4 ? 4 : 128; }
+inline int lane_k_batch(int L) {
+  const char* e = std::getenv("PT_LANE_K_BATCH");  // tuning knob
+  if (e) return std::atoi(e);
+  return L == 4 ? 4 : 128;
+}
 
 struct HostPlan {
   int n = 0, N = 0, L = 1;
