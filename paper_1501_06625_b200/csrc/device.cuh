@@ -1112,8 +1112,67 @@ __device__ __noinline__ void mgs(const DevPlan& P, const Work& W, const Team& te
 // Back substitution R dx = y, dx_k = (y_k - sum_{j>k} r_kj dx_j) * (1/r_kk),
 // column-oriented in one CTA with the next column of R prefetched one step
 // ahead (L2 latency off the dependency chain); then u = max|dx|, x += dx.
+// Component-split back substitution for n <= kThreads / 2 (the group-MGS
+// path, i.e. QD): thread 2i handles the real, 2i+1 the imaginary part of row
+// i, so each thread does half of every complex product on the chain.  The
+// operations are the complex ones, split: c_mul(a, b) = (a.re b.re - a.im
+// b.im, a.re b.im + a.im b.re) with r_sub(p, q) = r_add(p, -q), c_scale and
+// c_sub component-wise -- the same bits.  Operands are chosen by select so
+// both threads of a pair run one instruction stream.
+template <class R>
+__device__ __noinline__ double backsub_split(const DevPlan& P, const Work& W, Smem<R>& sh) {
+  constexpr int L = limbs_of<R>::L;
+  const int n = P.n;
+  const long SR = (long)n * (n + 1);
+  const int i = threadIdx.x >> 1;
+  const bool im = threadIdx.x & 1;
+  const bool row = i < n;
+  auto comp = [&](const cplx<R>& z) { return im ? z.im : z.re; };
+  R acc = rconst<R>(0.0), inv = rconst<R>(0.0);
+  cplx<R> cur = c_zero<R>();
+  if (row) {
+    acc = comp(load_c<R>(W.Rm, SR, (long)n * n + i));
+    inv = load_r<R>(W.inv, n, i);
+    cur = load_c<R>(W.Rm, SR, (long)(n - 1) * n + i);  // R column storage covers rows 0..n-1
+  }
+  for (int j = n - 1; j >= 0; --j) {
+    if (i == j) {
+      acc = r_mul(acc, inv);  // row j finished: this component of dx_j
+      if (im)
+        sh.xbs[j & 1].im = acc;
+      else
+        sh.xbs[j & 1].re = acc;
+    }
+    const cplx<R> nxt = row ? load_c<R>(W.Rm, SR, (long)(j > 0 ? j - 1 : 0) * n + i) : c_zero<R>();
+    __syncthreads();
+    const cplx<R> xj = sh.xbs[j & 1];
+    if (i < j) {
+      const R p1 = r_mul(cur.re, im ? xj.im : xj.re);
+      const R p2 = r_mul(cur.im, im ? xj.re : xj.im);
+      const R m = r_add(p1, im ? p2 : r_neg(p2));
+      acc = r_sub(acc, m);
+    }
+    cur = nxt;
+  }
+  double u = 0.0;
+  const double other = __shfl_xor_sync(0xffffffffu, r_hi(acc), 1);
+  if (row) {
+    if (!im) u = glibc_hypot(r_hi(acc), other);  // modulus_double of dx_i
+#pragma unroll
+    for (int l = 0; l < L; ++l) W.dx[(im ? L + l : l) * (long)n + i] = r_limb(acc, l);
+    R xv;
+#pragma unroll
+    for (int l = 0; l < L; ++l) r_set_limb(xv, l, W.x[(im ? L + l : l) * (long)n + i]);
+    const R xs = r_add(xv, acc);
+#pragma unroll
+    for (int l = 0; l < L; ++l) W.x[(im ? L + l : l) * (long)n + i] = r_limb(xs, l);
+  }
+  return block_nan_max(u, sh.red);
+}
+
 template <class R>
 __device__ __noinline__ double backsub_update(const DevPlan& P, const Work& W, Smem<R>& sh) {
+  if (P.n <= kThreads / 2) return backsub_split<R>(P, W, sh);
   const int n = P.n;
   const long SR = (long)n * (n + 1);
   cplx<R> acc[kMaxRowsPerThread], cur[kMaxRowsPerThread], nxt[kMaxRowsPerThread];
