@@ -18,6 +18,16 @@ using namespace ptdev;
 #endif
 using R = MB_R;
 
+// I-cache polluter: a long straight-line body (QD arithmetic, ~tens of KB of
+// code) run by every thread between two MGS sweeps when MB_POLLUTE is set
+__device__ __noinline__ double pollute(double seed) {
+  qd a{{seed, 1e-17, 1e-34, 1e-51}}, b{{1.0000001, 1e-20, 1e-37, 1e-54}};
+  cplx<qd> z{a, b}, u{b, a};
+#pragma unroll
+  for (int i = 0; i < 6; ++i) z = c_add(c_mul(z, u), z);
+  return z.re.c[0];
+}
+
 __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* A0, int reps, double* out, int probe) {
   __shared__ Smem<R> sh;
   __shared__ uint32_t s_flags[kMaxCols];
@@ -40,7 +50,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* 
       W.A[q] = A0[q];
     team.sync(&sh.flag);
     if (r == 1) t0 = gtimer();
-    if (std::is_same<R, dd>::value && probe && team.block == 0 && threadIdx.x >= 192 && threadIdx.x < 224) {
+    if (std::is_same<R, dd>::value && probe == 1 && team.block == 0 && threadIdx.x >= 192 && threadIdx.x < 224) {
 #ifndef MB_NO_DD_PROBES
       // concurrent probe: warp 6 of CTA 0 (no columns) runs the isolated
       // projection loop on a private smem slot while the MGS runs
@@ -58,6 +68,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mgs(DevPlan P, Work W, double* 
     } else
     mgs_warp<R, ClusterTeam>(P, W, team, sh, dyn, 1000ull + r, 0x1p-52);
     team.sync(&sh.flag);
+    if (probe == 2) out[4 + (threadIdx.x & 3)] = pollute(1.0 + r);
     if (threadIdx.x == 0) ++sh.mgs_seq;
     team.sync(&sh.flag);
   }
