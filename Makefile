@@ -1,5 +1,9 @@
-# Build the product library (CUDA, sm_100a) and the CPU oracle.
-#   make            -> paper_1501_06625_b200/libpathtrack_b200.so + oracle/liborc.so
+# Build the product library (CUDA, sm_100a), the host-only inputs library and
+# the CPU oracle.
+#   make            -> paper_1501_06625_b200/libpathtrack_b200.so   (the tracker: C-ABI + kernels)
+#                      paper_1501_06625_b200/libpt_inputs.so        (host: generators, system/solution
+#                                                                    files, Pieri minors; no CUDA)
+#                      oracle/liborc.so                             (test infrastructure)
 #   make ref        -> oracle/_ref/liborc_ref.so (needs /root/reference)
 NVCC     ?= /usr/local/cuda/bin/nvcc
 HOSTCXX  := $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo g++)
@@ -7,21 +11,30 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 # --fmad=false + explicit _rn intrinsics: no FMA contraction anywhere (bit parity)
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -ccbin $(HOSTCXX) \
             -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills --split-compile=0 $(EXTRA_NVFLAGS)
+HOSTFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wno-unknown-pragmas
 PKG      := paper_1501_06625_b200
 SRC      := $(PKG)/csrc
 LIB      := $(PKG)/libpathtrack_b200.so
-HDRS     := $(SRC)/mp.cuh $(SRC)/device.cuh $(SRC)/mgs_warp.cuh $(SRC)/plan.hpp $(SRC)/work.hpp include/pathtrack_b200.h
+INLIB    := $(PKG)/libpt_inputs.so
+HDRS     := $(SRC)/mp.cuh $(SRC)/device.cuh $(SRC)/mgs_warp.cuh $(SRC)/plan.hpp $(SRC)/work.hpp \
+            $(SRC)/kernels.cuh $(SRC)/kernel_set.hpp include/pathtrack_b200.h
+# one translation unit per precision: the three ptxas runs proceed in parallel
+KOBJS    := $(SRC)/kern_d.o $(SRC)/kern_dd.o $(SRC)/kern_qd.o $(SRC)/kern_misc.o $(SRC)/tracker.o
+INOBJS   := $(SRC)/gen.o $(SRC)/sysio.o $(SRC)/pieri.o
 
-all: $(LIB) oracle
+all: $(LIB) $(INLIB) oracle
 
-$(SRC)/tracker.o: $(SRC)/tracker.cu $(HDRS)
+$(SRC)/%.o: $(SRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(SRC)/gen.o: $(SRC)/gen.cpp $(SRC)/mp.cuh include/pathtrack_b200.h
-	$(HOSTCXX) -std=c++20 -O2 -fPIC -ffp-contract=off -c $< -o $@
+$(SRC)/%.o: $(SRC)/%.cpp $(SRC)/mp.cuh $(SRC)/inputs.hpp include/pathtrack_inputs.h
+	$(HOSTCXX) $(HOSTFLAGS) -c $< -o $@
 
-$(LIB): $(SRC)/tracker.o $(SRC)/gen.o
+$(LIB): $(KOBJS)
 	$(NVCC) $(ARCH) -shared -ccbin $(HOSTCXX) -o $@ $^
+
+$(INLIB): $(INOBJS)
+	$(HOSTCXX) -shared -o $@ $^
 
 oracle:
 	$(MAKE) -C oracle
@@ -30,7 +43,7 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -f $(SRC)/*.o $(LIB)
+	rm -f $(SRC)/*.o $(LIB) $(INLIB)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle ref clean

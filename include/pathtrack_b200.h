@@ -61,7 +61,8 @@ enum {
 
 /* Path status and failure kinds. */
 enum { PT_PATH_SUCCESS = 0, PT_PATH_FAIL = 1 };
-enum { PT_FAIL_NONE = 0, PT_FAIL_START = 1, PT_FAIL_MAX_STEPS = 2, PT_FAIL_MIN_STEP = 3 };
+enum { PT_FAIL_NONE = 0, PT_FAIL_START = 1, PT_FAIL_MAX_STEPS = 2, PT_FAIL_MIN_STEP = 3,
+       PT_FAIL_ABORT = 4 /* device watchdog: a barrier or MGS exchange stalled (not a SPEC outcome) */ };
 
 /* One polynomial system in canonical distributed form.
  * Equation i owns terms [eq_ptr[i], eq_ptr[i+1]); term t owns the
@@ -211,20 +212,9 @@ int pt_arith_host(pt_prec prec, int32_t op, int64_t count, const double* a, cons
 const char* pt_last_error(void);
 const char* pt_version(void);
 
-/* ---- synthetic inputs (BASELINE.json configs) ---------- */
-typedef struct pt_sysbuf pt_sysbuf;
-int pt_gen_cyclic(int32_t n, pt_prec prec, pt_sysbuf** out);
-int pt_gen_augment(const pt_sysbuf* f, int32_t dim, uint64_t seed, pt_prec prec, pt_sysbuf** out);
-int pt_gen_chandra(int32_t n, double c, pt_prec prec, pt_sysbuf** out);
-int pt_gen_random_dense(int32_t n, int32_t degree, int32_t n_monomials, uint64_t seed, pt_prec prec,
-                        pt_sysbuf** out);
-int pt_gen_total_degree(int32_t n, int32_t degree, pt_prec prec, pt_sysbuf** out);
-int pt_sysbuf_desc(const pt_sysbuf* s, pt_system_desc* out);
-void pt_sysbuf_free(pt_sysbuf* s);
-/* Rng(seed).unit<R>() (rng.hpp:38-41): 2L limbs. */
-int pt_gen_gamma(uint64_t seed, pt_prec prec, double* out);
-/* unit_complex<R>(theta) (complex.hpp:141-148): 2L limbs. */
-int pt_gen_unit_complex(double theta, pt_prec prec, double* out);
+/* Inputs (synthetic systems, system / solution files, Pieri minors) live in
+ * the host-only library declared in pathtrack_inputs.h: building the inputs
+ * never loads this library. */
 
 #ifdef __cplusplus
 }

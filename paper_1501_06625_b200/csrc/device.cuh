@@ -277,9 +277,13 @@ struct ClusterTeam {
         return (int)(v & 1u);
       }
       if (++spins > 512u) __nanosleep(20);
-      if ((spins & 1023u) == 0 && (double)(gtimer() - t0) > kTimeoutNs) {
+      // Watchdog: a stalled exchange sets CTL_ABORT and gives up; every other
+      // waiter sees the flag and gives up too, all CTAs still reach the next
+      // cluster barrier (no CTA exits early, no __trap poisoning the context)
+      // and newton() reports NW_ABORT after it.
+      if ((spins & 1023u) == 0 && (ld_acquire(ctl + CTL_ABORT) || (double)(gtimer() - t0) > kTimeoutNs)) {
         atomicExch(ctl + CTL_ABORT, 1ull);
-        __trap();  // hardware cluster barriers cannot be abandoned: kill the launch instead of hanging
+        return -1;
       }
     }
   }
@@ -299,13 +303,20 @@ struct BlockTeam {
     __threadfence_block();
     *(volatile uint32_t*)(sflags + k) = ((uint32_t)(epoch & 0x7fffffffull) << 1) | (uint32_t)fail;
   }
+  // Flags are cleared at the start of every path (k_track_batch), so the low
+  // 31 bits of the epoch only have to be unique within one path.
   __device__ int wait(const unsigned long long*, int k, unsigned long long epoch) const {
     const uint32_t want = (uint32_t)(epoch & 0x7fffffffull);
-    for (;;) {
+    const unsigned long long t0 = gtimer();
+    for (unsigned int spins = 1;; ++spins) {
       const uint32_t v = *(volatile uint32_t*)(sflags + k);
       if ((v >> 1) == want) {
         __threadfence_block();
         return (int)(v & 1u);
+      }
+      if ((spins & 1023u) == 0 && (ld_acquire(ctl + CTL_ABORT) || (double)(gtimer() - t0) > kTimeoutNs)) {
+        atomicExch(ctl + CTL_ABORT, 1ull);
+        return -1;
       }
     }
   }
@@ -411,7 +422,7 @@ __device__ __forceinline__ double nan_max(double a, double b) {
 }
 
 // block-wide NaN-propagating max; every thread gets the result
-__device__ double block_nan_max(double v, double* s_red) {
+__device__ inline double block_nan_max(double v, double* s_red) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = nan_max(v, __shfl_xor_sync(0xffffffffu, v, off));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1339,6 +1350,9 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     pc.lap(W.prof + PROF_MGS);
     if (threadIdx.x == 0) ++sh.mgs_seq;  // read again only after the next team barrier
+    // a watchdog inside the MGS exchange (cluster / block teams) set CTL_ABORT
+    // before its CTA arrived at the barrier above: every CTA sees it here
+    if (!Team::kGrid && ld_acquire(W.ctl + CTL_ABORT)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
     if (ld_acquire(W.ctl + CTL_RANK) == epoch) {
       o.kind = NW_LINEAR_SOLVE;
       return o;
@@ -1385,9 +1399,23 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
   pt_path_stats st{};
   if (leader)
     for (int i = threadIdx.x; i < n; i += kThreads) store_c<R>(W.x, n, i, load_c<R>(io.start, n, i));
-  if (!team.sync(&sh.flag)) return;
+  // Watchdog abort (stalled barrier / exchange): the path is reported as
+  // failed with PT_FAIL_ABORT -- never left with stale statistics.
+  auto aborted = [&](int iters) {
+    if (leader && threadIdx.x == 0) {
+      pt_path_stats a{};
+      a.status = PT_PATH_FAIL;
+      a.failure_kind = PT_FAIL_ABORT;
+      a.newton_iters = st.newton_iters + iters;
+      a.final_residual = bitsd(0x7ff8000000000000ull);
+      a.final_update = bitsd(0x7ff8000000000000ull);
+      *io.stats = a;
+      if (io.trace_len) *io.trace_len = 0;
+    }
+  };
+  if (!team.sync(&sh.flag)) return aborted(0);
   NewtonOut o = newton<R, Team>(P, W, team, sh, colsm, sp, 0.0, epoch);
-  if (o.kind == NW_ABORT) return;
+  if (o.kind == NW_ABORT) return aborted(o.iters);
   st.start_iters = o.iters;
   st.newton_iters = o.iters;
   st.solves = o.solves;
@@ -1419,10 +1447,10 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
       const double ttrial = tsum < 1.0 ? tsum : 1.0;
       PhaseClock pc(leader && threadIdx.x == 0 && W.prof != nullptr);
       if (leader) predict<R>(P, W, H, ttrial);
-      if (!team.sync(&sh.flag)) return;
+      if (!team.sync(&sh.flag)) return aborted(0);
       pc.lap(W.prof + PROF_PREDICT);
       o = newton<R, Team>(P, W, team, sh, colsm, sp, ttrial, epoch);
-      if (o.kind == NW_ABORT) return;
+      if (o.kind == NW_ABORT) return aborted(o.iters);
       st.newton_iters += o.iters;
       st.solves += o.solves;
       st.final_residual = o.residual;

@@ -19,84 +19,12 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
-#include "../../include/pathtrack_b200.h"
-#include "mp.cuh"
-
-struct pt_sysbuf {
-  int32_t n_vars = 0, n_eqs = 0, L = 1;
-  std::vector<int32_t> eq_ptr, term_ptr, var, exp;
-  std::vector<double> coef;  // [2][L][n_terms]
-};
+#include "inputs.hpp"
 
 namespace ptgen {
-
-using Support = std::vector<std::pair<int, int>>;  // (var, exp), var ascending
-
-struct Term {
-  Support sup;
-  double c[8];  // re limbs then im limbs (2L used)
-};
-
-class Rng {  // rng.hpp:14-45
- public:
-  explicit Rng(uint64_t seed) : g_(seed) {}
-  uint64_t bits() { return g_(); }
-  double uniform01() { return static_cast<double>(g_() >> 11) * 0x1p-53; }
-  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform01(); }
-  double angle() { return 2.0 * std::numbers::pi * uniform01(); }
-
- private:
-  std::mt19937_64 g_;
-};
-
-inline int limbs(pt_prec p) { return p == PT_D ? 1 : (p == PT_DD ? 2 : 4); }
-
-// canonical form: terms sorted lexicographically by support
-pt_sysbuf* emit(int n, std::vector<std::vector<Term>>& eqs, int L) {
-  auto* s = new pt_sysbuf;
-  s->n_vars = n;
-  s->n_eqs = (int)eqs.size();
-  s->L = L;
-  s->eq_ptr.push_back(0);
-  s->term_ptr.push_back(0);
-  std::vector<const Term*> all;
-  for (auto& e : eqs) {
-    std::stable_sort(e.begin(), e.end(), [](const Term& a, const Term& b) { return a.sup < b.sup; });
-    for (auto& t : e) {
-      for (auto& ve : t.sup) {
-        s->var.push_back(ve.first);
-        s->exp.push_back(ve.second);
-      }
-      s->term_ptr.push_back((int)s->var.size());
-      all.push_back(&t);
-    }
-    s->eq_ptr.push_back((int)all.size());
-  }
-  const long T = (long)all.size();
-  s->coef.assign((size_t)2 * L * T, 0.0);
-  for (long t = 0; t < T; ++t)
-    for (int q = 0; q < 2 * L; ++q) s->coef[(size_t)q * T + t] = all[t]->c[q];
-  return s;
-}
-
-template <class R>
-void put(Term& t, const ptk::cplx<R>& v) {
-  constexpr int L = ptk::limbs_of<R>::L;
-  for (int l = 0; l < L; ++l) {
-    t.c[l] = ptk::r_limb(v.re, l);
-    t.c[L + l] = ptk::r_limb(v.im, l);
-  }
-}
-Term make_term(Support sup, double re, double im, int L) {
-  Term t;
-  t.sup = std::move(sup);
-  std::memset(t.c, 0, sizeof t.c);
-  t.c[0] = re;
-  t.c[L] = im;
-  return t;
-}
 
 template <class R>
 pt_sysbuf* chandra(int n, double c) {
@@ -264,6 +192,55 @@ int pt_sysbuf_desc(const pt_sysbuf* s, pt_system_desc* d) {
 }
 
 void pt_sysbuf_free(pt_sysbuf* s) { delete s; }
+
+const char* pt_inputs_last_error(void) { return g_err.c_str(); }
+void pt_text_free(char* text) { std::free(text); }
+
+int pt_sysbuf_from_desc(const pt_system_desc* d, pt_prec prec, pt_sysbuf** out) {
+  if (!d || !out || d->n_vars < 0 || d->n_eqs < 0 || d->n_terms < 0) return fail(PT_E_INVAL, "bad system descriptor");
+  pt_sysbuf tmp;
+  tmp.n_vars = d->n_vars;
+  tmp.n_eqs = d->n_eqs;
+  tmp.L = limbs(prec);
+  tmp.eq_ptr.assign(d->eq_ptr, d->eq_ptr + d->n_eqs + 1);
+  tmp.term_ptr.assign(d->term_ptr, d->term_ptr + d->n_terms + 1);
+  const int V = tmp.term_ptr.back();
+  tmp.var.assign(d->var, d->var + V);
+  tmp.exp.assign(d->exp, d->exp + V);
+  tmp.coef.assign(d->coef, d->coef + (size_t)2 * tmp.L * d->n_terms);
+  for (int q = 0; q < V; ++q)
+    if (tmp.var[q] < 0 || tmp.var[q] >= d->n_vars || tmp.exp[q] < 1) return fail(PT_E_INVAL, "bad term support");
+  auto eqs = terms_of(tmp);
+  canonicalize(eqs, tmp.L);
+  *out = emit(d->n_vars, eqs, tmp.L);
+  return PT_OK;
+}
+
+int pt_sysbuf_stack(const pt_sysbuf* a, const pt_sysbuf* b, pt_sysbuf** out) {
+  if (!a || !b || !out || a->n_vars != b->n_vars || a->L != b->L) return fail(PT_E_INVAL, "cannot stack systems");
+  auto ea = terms_of(*a), eb = terms_of(*b);
+  ea.insert(ea.end(), eb.begin(), eb.end());
+  *out = emit(a->n_vars, ea, a->L);
+  return PT_OK;
+}
+
+// Table 5: n = l m^2, m >= 2 maximal, l squarefree;
+// dimension m - 1, degree m.
+int pt_cyclic_degree(int32_t n, int32_t* m, int32_t* l, int32_t* dim, int32_t* degree) {
+  if (n < 1) return fail(PT_E_INVAL, "n must be >= 1");
+  int best = 1;
+  for (int q = 2; (long)q * q <= n; ++q)
+    if (n % (q * q) == 0) best = q;
+  if (best < 2) return 0;
+  int rest = n / (best * best);
+  for (int q = 2; (long)q * q <= rest; ++q)
+    if (rest % (q * q) == 0) return 0;  // unreachable for maximal m, kept for clarity
+  if (m) *m = best;
+  if (l) *l = rest;
+  if (dim) *dim = best - 1;
+  if (degree) *degree = best;
+  return 1;
+}
 
 int pt_gen_unit_complex(double theta, pt_prec prec, double* out) {
   if (!out) return PT_E_INVAL;

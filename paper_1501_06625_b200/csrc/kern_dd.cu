@@ -1,0 +1,7 @@
+// kern_dd.cu -- the tracker kernels instantiated for R = ptk::dd (see kernels.cuh).
+#include "kernels.cuh"
+
+const ptdev::KernelSet ptdev::kset_dd = {
+    (const void*)&ptdev::k_track_grid<ptk::dd>,  (const void*)&ptdev::k_track_cluster<ptk::dd>,
+    (const void*)&ptdev::k_track_batch<ptk::dd>, (const void*)&ptdev::k_eval<ptk::dd>,
+    (const void*)&ptdev::k_lstsq<ptk::dd>,       (const void*)&ptdev::k_arith<ptk::dd>};

@@ -112,16 +112,18 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, int parity) {
       : "memory");
   return ok != 0;
 }
-// Wait for phase `parity` of a receive barrier; a stalled exchange traps
-// (cluster barriers cannot be abandoned) after the watchdog time.
-__device__ __forceinline__ void mbar_wait(uint64_t* b, int parity, unsigned long long* ctl) {
-  if (mbar_try(b, parity)) return;
+// Wait for phase `parity` of a receive barrier.  Watchdog: a stalled
+// exchange (or an abort raised by another waiter) sets CTL_ABORT and returns
+// false; the caller abandons the sweep and newton() reports NW_ABORT after
+// the team barrier (no __trap: the CUDA context stays usable).
+__device__ __forceinline__ bool mbar_wait(uint64_t* b, int parity, unsigned long long* ctl) {
+  if (mbar_try(b, parity)) return true;
   const unsigned long long t0 = gtimer();
   for (unsigned int spins = 1;; ++spins) {
-    if (mbar_try(b, parity)) return;
-    if ((spins & 1023u) == 0 && (double)(gtimer() - t0) > kTimeoutNs) {
+    if (mbar_try(b, parity)) return true;
+    if ((spins & 1023u) == 0 && (ld_acquire(ctl + CTL_ABORT) || (double)(gtimer() - t0) > kTimeoutNs)) {
       atomicExch(ctl + CTL_ABORT, 1ull);
-      __trap();
+      return false;
     }
   }
 }
@@ -400,7 +402,7 @@ struct WarpMgs {
       if (mine) {
         load_col(slot_ptr(kls), N, q);
       } else if constexpr (MB) {
-        mbar_wait(bars() + k, par, W.ctl);
+        if (!__all_sync(0xffffffffu, mbar_wait(bars() + k, par, W.ctl))) return;  // watchdog abort
         if (kc == c) {  // the owner's slot in this CTA
           load_col(slot_ptr(kls), N, q);
           if (next_mine && lane == 0) prev = sh.pmax[k];

@@ -33,7 +33,7 @@
 #if defined(PT_QD_INLINE) && PT_QD_INLINE
 #define PT_QDOP __host__ __device__ __forceinline__
 #else
-#define PT_QDOP __host__ __device__ __noinline__
+#define PT_QDOP static __host__ __device__ __noinline__
 #endif
 #else
 #define PT_HD inline

@@ -1,11 +1,8 @@
-// tracker.cu -- kernels and the C-ABI (include/pathtrack_b200.h).
-//
-//   k_track_grid<R>   one path, cooperative persistent grid (GridTeam)
-//   k_track_batch<R>  many paths, one CTA per path, atomic path queue
-//   k_eval<R>         evaluate_homotopy only (parity tests)
-//   k_lstsq<R>        least_squares_solve only (parity tests)
-//   k_arith<R>        bulk scalar ops (arithmetic parity tests)
-// There is no host fallback: every compute entry point needs an sm_100 device.
+// tracker.cu -- the C-ABI (include/pathtrack_b200.h): plan compilation,
+// engine choice, launches.  The kernels live in kernels.cuh and are
+// instantiated per precision in kern_{d,dd,qd}.cu; they are launched here
+// through the KernelSet tables.  There is no host fallback: every compute
+// entry point needs an sm_100 device.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,7 +14,7 @@
 #include <string>
 #include <vector>
 
-#include "device.cuh"
+#include "kernels.cuh"
 #include "work.hpp"
 
 using namespace ptdev;
@@ -38,390 +35,27 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 inline int limbs(pt_prec p) { return p == PT_D ? 1 : (p == PT_DD ? 2 : 4); }
+inline const KernelSet& kset(pt_prec p) { return p == PT_D ? kset_d : (p == PT_DD ? kset_dd : kset_qd); }
 
-// Per-path workspace layout (element counts); slice b of a batch starts at
-// b * dslice doubles / b * uslice u64 words.
-struct Layout {
-  long x, hist, ws, A, Rm, inv, rmaxp, hmod, scal, dx, qg;  // double offsets
-  long dslice;
-  long flags, ctl, prof;  // u64 offsets
-  long uslice;
-};
-
-Layout make_layout(int L, int n, int N, long ws_len) {
-  Layout o{};
-  long d = 0;
-  auto take = [&](long cnt) {
-    long at = d;
-    d += (cnt + 31) & ~31L;  // 256-byte aligned sub-arrays
-    return at;
-  };
-  o.x = take(2L * L * n);
-  o.hist = take((long)(kMaxDegree + 1) * 2 * L * n);
-  o.ws = take(2L * L * ws_len);
-  o.A = take(2L * L * N * (n + 1));
-  o.Rm = take(2L * L * n * (n + 1));
-  o.inv = take((long)L * n);
-  o.rmaxp = take(n);
-  o.hmod = take(N);
-  o.scal = take(8);
-  o.dx = take(2L * L * n);
-  o.qg = take((long)n * mgs_warp_qs(L, N));
-  o.dslice = d;
-  long u = 0;
-  o.flags = u;
-  u += (n + 1 + 31) & ~31L;
-  o.ctl = u;
-  u += 32;
-  o.prof = u;
-  u += kProfSlots + 14 * (n + 2) + 32;  // + per-column fine markers (PT_MGS_FINE builds)
-  o.uslice = u;
-  return o;
-}
-
-__host__ __device__ inline Work carve(double* dbase, unsigned long long* ubase, const Layout& o, long b) {
-  double* d = dbase + b * o.dslice;
-  unsigned long long* u = ubase + b * o.uslice;
-  Work W;
-  W.x = d + o.x;
-  W.hist = d + o.hist;
-  W.ws = d + o.ws;
-  W.A = d + o.A;
-  W.Rm = d + o.Rm;
-  W.inv = d + o.inv;
-  W.rmaxp = d + o.rmaxp;
-  W.hmod = d + o.hmod;
-  W.scal = d + o.scal;
-  W.dx = d + o.dx;
-  W.qg = d + o.qg;
-  W.flags = u + o.flags;
-  W.ctl = u + o.ctl;
-  W.prof = u + o.prof;
-  return W;
+// Launch a kernel (as a cluster of `cluster` CTAs when cluster > 0) from its
+// untyped pointer.
+cudaError_t launch_ex(const void* fn, int grid, size_t smem, cudaStream_t s, int cluster, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = cluster > 0 ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 }  // namespace
-
-// ---------------------------------------------------------------------------
-// kernels
-// ---------------------------------------------------------------------------
-// Per-launch CTA prologue: MGS sweep counter and, for the mbarrier exchange
-// of the warp MGS, one receive barrier per column (phase = sweep parity).
-// The caller's team barrier publishes the initialisation.
-template <class R>
-__device__ void cta_prologue(const DevPlan& P, Smem<R>& sh, double* dyn_smem, int nblocks) {
-  if (threadIdx.x == 0) {
-    sh.mgs_seq = 0;
-    if (P.mgs_warp == 2) {
-      constexpr int L = limbs_of<R>::L;
-      uint64_t* bars = reinterpret_cast<uint64_t*>(dyn_smem + mgs_warp_slots_doubles(L, P.N, P.n, nblocks) +
-                                                   (long)P.n * mgs_warp_qs(L, P.N));
-      for (int k = 0; k < P.n; ++k) mbar_init(bars + k, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-  }
-}
-
-template <class R>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_track_grid(DevPlan P, Work W, pt_step_params sp, TrackIO io, unsigned long long epoch_base) {
-  __shared__ Smem<R> sh;
-  extern __shared__ double dyn_smem[];
-  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
-  cta_prologue<R>(P, sh, dyn_smem, (int)gridDim.x);
-  __syncthreads();
-  track_path<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
-}
-
-// One path on one thread-block cluster (launched with a cluster dimension
-// attribute, grid == cluster): barrier.cluster + DSMEM column exchange.
-template <class R>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_track_cluster(DevPlan P, Work W, pt_step_params sp, TrackIO io, unsigned long long epoch_base) {
-  __shared__ Smem<R> sh;
-  __shared__ uint32_t s_flags[kMaxCols];
-  extern __shared__ double dyn_smem[];
-  for (int i = threadIdx.x; i < kMaxCols; i += kThreads) s_flags[i] = 0;
-  const ClusterTeam team{W.ctl, (int)cluster_nranks(), (int)cluster_rank(), s_flags};
-  cta_prologue<R>(P, sh, dyn_smem, team.nblocks);
-  team.sync(&sh.flag);
-  track_path<R, ClusterTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
-  team.sync(&sh.flag);  // keep every CTA's shared memory alive until all DSMEM reads are done
-}
-
-// Batch CTAs per SM: two paths share an SM in D / DD (128 registers per
-// thread suffice there); QD keeps the whole register file for one path.
-#ifndef PT_BATCH_CTAS
-#define PT_BATCH_CTAS 2
-#endif
-template <class R>
-constexpr int kBatchCtasPerSm = limbs_of<R>::L == 4 ? 1 : PT_BATCH_CTAS;
-
-template <class R>
-__global__ void __launch_bounds__(kThreads, kBatchCtasPerSm<R>)
-    k_track_batch(DevPlan P, double* dbase, unsigned long long* ubase, Layout lay, pt_step_params sp,
-                  const double* starts, double* ends, pt_path_stats* stats, int n_paths,
-                  unsigned long long* queue, unsigned long long epoch_base) {
-  __shared__ Smem<R> sh;
-  __shared__ int s_path;
-  __shared__ uint32_t s_flags[kMaxCols];
-  extern __shared__ double dyn_smem[];
-  for (int i = threadIdx.x; i < kMaxCols; i += kThreads) s_flags[i] = 0;
-  const Work W = carve(dbase, ubase, lay, blockIdx.x);
-  const BlockTeam team{W.ctl, 1, 0, s_flags};
-  cta_prologue<R>(P, sh, dyn_smem, 1);
-  __syncthreads();
-  const long PS = 2L * limbs_of<R>::L * P.n;
-  for (;;) {
-    if (threadIdx.x == 0) s_path = (int)atomicAdd(queue, 1ull);
-    __syncthreads();
-    const int p = s_path;
-    __syncthreads();
-    if (p >= n_paths) break;
-    TrackIO io{starts + p * PS, ends + p * PS, stats + p, nullptr, 0, nullptr};
-    track_path<R, BlockTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io,
-                             epoch_base + ((unsigned long long)p << 16));
-  }
-}
-
-template <class R>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_eval(DevPlan P, Work W, const double* x, double t, double* h, double* J, double* rmax) {
-  __shared__ Smem<R> sh;
-  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
-  const int n = P.n, N = P.N;
-  if (team.block == 0)
-    for (int i = threadIdx.x; i < n; i += kThreads) store_c<R>(W.x, n, i, load_c<R>(x, n, i));
-  if (!team.sync(&sh.flag)) return;
-  eval_monomials<R>(P, W, W.x, team.block * kThreads + threadIdx.x, team.nblocks * kThreads);
-  if (!team.sync(&sh.flag)) return;
-  eval_slots<R, GridTeam>(P, W, team, sh, t);
-  if (!team.sync(&sh.flag)) return;
-  const long SA = (long)N * (n + 1), SJ = (long)N * n;
-  const long tid = (long)team.block * kThreads + threadIdx.x, nth = (long)team.nblocks * kThreads;
-  if (J)
-    for (long q = tid; q < SJ; q += nth) store_c<R>(J, SJ, q, load_c<R>(W.A, SA, q));
-  if (h)
-    for (long i = tid; i < N; i += nth) store_c<R>(h, N, i, c_neg(load_c<R>(W.A, SA, (long)n * N + i)));
-  if (team.block == 0) {
-    double r = 0.0;
-    for (int i = threadIdx.x; i < N; i += kThreads) r = nan_max(r, W.hmod[i]);
-    r = block_nan_max(r, sh.red);
-    if (threadIdx.x == 0 && rmax) *rmax = r;
-  }
-}
-
-template <class R>
-__global__ void __launch_bounds__(kThreads, 1) k_lstsq(DevPlan P, Work W, unsigned long long epoch, int* status) {
-  __shared__ Smem<R> sh;
-  extern __shared__ double dyn_smem[];
-  const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
-  cta_prologue<R>(P, sh, dyn_smem, (int)gridDim.x);
-  __syncthreads();
-  mgs<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, nullptr, epoch, kSqrtEps<R>());
-  if (!team.sync(&sh.flag)) {
-    if (team.block == 0 && threadIdx.x == 0) *status = PT_E_TIMEOUT;
-    return;
-  }
-  if (ld_acquire(W.ctl + CTL_RANK) == epoch) {
-    if (team.block == 0 && threadIdx.x == 0) *status = PT_E_RANK;
-    return;
-  }
-  if (team.block == 0) {
-    backsub_update<R>(P, W, sh);
-    if (threadIdx.x == 0) *status = 0;
-  }
-}
-
-template <class R>
-__device__ R arith_rd(const double* p) {
-  R v;
-#pragma unroll
-  for (int l = 0; l < limbs_of<R>::L; ++l) r_set_limb(v, l, p[l]);
-  return v;
-}
-template <class R>
-__host__ __device__ inline void arith_one(int op, const double* pa, const double* pb, double* po) {
-  constexpr int L = limbs_of<R>::L;
-  auto rd = [](const double* p) {
-    R v;
-    for (int l = 0; l < L; ++l) r_set_limb(v, l, p[l]);
-    return v;
-  };
-  auto wr = [](const R& v, double* p) {
-    for (int l = 0; l < L; ++l) p[l] = r_limb(v, l);
-  };
-  const R ar = rd(pa), br = rd(pb);
-  const cplx<R> ac{rd(pa), rd(pa + L)}, bc{rd(pb), rd(pb + L)};
-  cplx<R> oc;
-  switch (op) {
-    case 0: wr(r_add(ar, br), po); break;
-    case 1: wr(r_sub(ar, br), po); break;
-    case 2: wr(r_mul(ar, br), po); break;
-    case 3: wr(r_mul_d(ar, pb[0]), po); break;
-    case 4: wr(r_div(ar, br), po); break;
-    case 5: wr(r_sqrt(ar), po); break;
-    case 6:
-      if constexpr (L == 4) {
-        wr(qd_renormalize(ar), po);
-      } else if constexpr (L == 2) {
-        wr(dd_norm(r_limb(ar, 0), r_limb(ar, 1)), po);
-      } else {
-        wr(ar, po);
-      }
-      break;
-    case 7: oc = c_mul(ac, bc); wr(oc.re, po); wr(oc.im, po + L); break;
-    case 8: oc = c_add(ac, bc); wr(oc.re, po); wr(oc.im, po + L); break;
-    case 9: oc = c_conj_mul(ac, bc); wr(oc.re, po); wr(oc.im, po + L); break;
-    case 10: wr(c_norm_sqr(ac), po); break;
-    case 11: po[0] = c_mod_double(ac); break;
-    case 12: wr(r_powi(ar, (unsigned)pb[0]), po); break;
-    case 14: oc = c_scale(ac, br); wr(oc.re, po); wr(oc.im, po + L); break;
-    case 15: oc = c_powi(ac, (unsigned)pb[0]); wr(oc.re, po); wr(oc.im, po + L); break;
-    default: break;
-  }
-}
-
-template <class R>
-__global__ void k_arith(int op, long count, const double* a, const double* b, double* out) {
-  constexpr int L = limbs_of<R>::L;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
-    arith_one<R>(op, a + i * 2 * L, b + i * 2 * L, out + i * 2 * L);
-}
-
-// FP64-pipe peak: kPeakChains independent DFMA chains per thread.
-constexpr int kPeakChains = 8;
-__global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters) {
-  double a[kPeakChains];
-#pragma unroll
-  for (int c = 0; c < kPeakChains; ++c) a[c] = 1e-3 * (threadIdx.x + c);
-  const double b = 0.9999999, d = 1e-9;
-  for (int i = 0; i < iters; ++i) {
-#pragma unroll
-    for (int c = 0; c < kPeakChains; ++c) a[c] = __fma_rn(a[c], b, d);
-  }
-  double s = 0;
-#pragma unroll
-  for (int c = 0; c < kPeakChains; ++c) s += a[c];
-  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-}
-
-// Latency microbenchmarks (one thread): dependent chains of the primitive and
-// emulated operations, in SM cycles per operation.
-__global__ void k_latency(double* out, double seed) {
-  const int T = 256;
-  long long c0, c1;
-  double a = seed, b = 1.0000001;
-  c0 = clock64();
-  for (int i = 0; i < T; ++i) a = __dadd_rn(a, b);
-  c1 = clock64();
-  out[0] = (double)(c1 - c0) / T;
-  out[10] = a;
-  dd x{seed, 0.0}, y{1.0000001, 1e-20};
-  c0 = clock64();
-  for (int i = 0; i < T; ++i) x = r_add(x, y);
-  c1 = clock64();
-  out[1] = (double)(c1 - c0) / T;
-  c0 = clock64();
-  for (int i = 0; i < T; ++i) x = r_mul(x, y);
-  c1 = clock64();
-  out[2] = (double)(c1 - c0) / T;
-  out[11] = x.hi;
-  qd q{{seed, 1e-17, 1e-34, 1e-51}}, w{{1.0000001, 1e-20, 1e-37, 1e-54}};
-  c0 = clock64();
-  for (int i = 0; i < T / 8; ++i) q = r_add(q, w);
-  c1 = clock64();
-  out[3] = (double)(c1 - c0) / (T / 8);
-  c0 = clock64();
-  for (int i = 0; i < T / 8; ++i) q = r_mul(q, w);
-  c1 = clock64();
-  out[4] = (double)(c1 - c0) / (T / 8);
-  out[12] = q.c[0];
-  cplx<dd> z{{seed, 0}, {0.5, 0}}, u{{0.9999, 1e-20}, {0.01, 0}};
-  c0 = clock64();
-  for (int i = 0; i < T; ++i) z = c_mul(z, u);
-  c1 = clock64();
-  out[5] = (double)(c1 - c0) / T;
-  out[13] = z.re.hi;
-  double h = seed;
-  c0 = clock64();
-  for (int i = 0; i < T; ++i) h = glibc_hypot(h, 0.5) * 0.5;
-  c1 = clock64();
-  out[6] = (double)(c1 - c0) / T;
-  out[14] = h;
-}
-
-// MGS building blocks on one warp (group width 1, N = 64), in cycles:
-// out[0] group_tree<cplx<dd>>, [1] mgs_project, [2] c_conj_mul, [3] dd sqrt, [4] dd div
-__global__ void k_mgs_pieces(double* out) {
-  __shared__ Smem<dd> sh;
-  __shared__ double col[4 * 64], rcol[4 * 65], invb[2];
-  const int lane = threadIdx.x;
-  const Group g{1, lane, 1};
-  for (int i = lane; i < 4 * 64; i += 32) col[i] = 1.0 + 1e-3 * i;
-  __syncwarp();
-  cplx<dd> q[kMaxElems];
-  for (int r = 0; r < 2; ++r) q[r] = cplx<dd>{{0.5 + 1e-4 * lane, 1e-20}, {0.25, 0}};
-  DevPlan P{};
-  P.n = 64;
-  P.N = 64;
-  P.P_mgs = 32;
-  P.mgs_gw = 1;
-  OwnedCol c{ColRef{col, 64}, ColRef{rcol, 65}, invb, 1, 0};
-  int phase = 0;
-  cplx<dd> acc{{1.0 + lane, 0}, {0.5, 0}};
-  long long t0 = clock64();
-  cplx<dd> t = group_tree(acc, g, 32, 64, sh.tree);
-  __syncwarp();
-  long long t1 = clock64();
-  mgs_project<dd, true>(P, g, 0, sh, phase, q, c, 3, 10);
-  __syncwarp();
-  long long t2 = clock64();
-  cplx<dd> z = c_conj_mul(q[0], q[1]);
-  long long t3 = clock64();
-  dd sq = r_sqrt(z.re);
-  long long t4 = clock64();
-  dd dv = r_div(dd{1.0, 0.0}, sq);
-  long long t5 = clock64();
-  if (lane == 0) {
-    out[0] = (double)(t1 - t0);
-    out[1] = (double)(t2 - t1);
-    out[2] = (double)(t3 - t2);
-    out[3] = (double)(t4 - t3);
-    out[4] = (double)(t5 - t4);
-    out[15] = t.re.hi + dv.hi + col[5];
-  }
-}
-
-// Grid barrier cost: every CTA crosses `iters` GridTeam barriers.
-__global__ void k_barrier(unsigned long long* ctl, int iters, double* out) {
-  __shared__ int flag;
-  const GridTeam team{ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
-  const unsigned long long t0 = gtimer();
-  for (int i = 0; i < iters; ++i)
-    if (!team.sync(&flag)) break;
-  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (double)(gtimer() - t0) / iters;
-}
-
-// Flag ping-pong between CTA 0 and CTA gridDim.x-1 (release/acquire through L2).
-__global__ void k_pingpong(unsigned long long* flags, int iters, double* out) {
-  if (threadIdx.x != 0) return;
-  const bool ping = blockIdx.x == 0, pong = blockIdx.x == gridDim.x - 1;
-  if (!ping && !pong) return;
-  const unsigned long long t0 = gtimer();
-  for (int i = 1; i <= iters; ++i) {
-    if (ping) {
-      st_release(flags, i);
-      while (ld_acquire(flags + 32) != (unsigned long long)i) {
-      }
-    } else {
-      while (ld_acquire(flags) != (unsigned long long)i) {
-      }
-      st_release(flags + 32, i);
-    }
-  }
-  if (ping) out[0] = (double)(gtimer() - t0) / iters / 2;  // one-way ns
-}
 
 // ---------------------------------------------------------------------------
 // plan object
@@ -469,10 +103,6 @@ struct pt_plan {
 
 namespace {
 
-template <class R>
-const void* grid_kernel() {
-  return reinterpret_cast<const void*>(&k_track_grid<R>);
-}
 
 int occupancy_blocks(const void* fn, int device, int* per_sm, int* sms) {
   cudaDeviceProp prop;
@@ -532,8 +162,8 @@ int set_dyn_smem(const void* fn, size_t bytes) {
   return PT_OK;
 }
 
-template <class R>
-int dispatch_grid_size(pt_plan* p, const void* fn) {
+int dispatch_grid_size(pt_plan* p) {
+  const void* fn = kset(p->prec).track_grid;
   int per_sm = 0, sms = 0;
   int rc = occupancy_blocks(fn, p->device, &per_sm, &sms);
   if (rc) return rc;
@@ -547,7 +177,7 @@ int dispatch_grid_size(pt_plan* p, const void* fn) {
   want = std::max(want, (long)(p->n + 1 + gpc_mgs - 1) / gpc_mgs);
   p->grid_blocks = (int)std::min<long>(want, std::min(cap, sms));
   p->grid_dyn_smem = engine_smem(p->L, p->N, p->n, p->grid_blocks, false, &p->grid_warp);
-  for (const void* f : {fn, (const void*)&k_eval<R>}) {
+  for (const void* f : {fn, kset(p->prec).eval}) {
     rc = set_dyn_smem(f, p->grid_dyn_smem);
     if (rc) return rc;
   }
@@ -559,9 +189,8 @@ int dispatch_grid_size(pt_plan* p, const void* fn) {
 
 // Largest cluster (<= 16 CTAs) the device can schedule for this kernel with
 // the MGS columns staged in shared memory.
-template <class R>
 int setup_cluster(pt_plan* p) {
-  const void* fn = (const void*)&k_track_cluster<R>;
+  const void* fn = kset(p->prec).track_cluster;
   PT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   p->cluster_size = 0;
   const char* ce = getenv("PT_CLUSTER_MAX");  // tuning knob: cap the cluster size
@@ -630,29 +259,30 @@ int stage_fits(const pt_plan* p, size_t dyn_bytes) {
 // the monomial evaluation can read x from a shared-memory copy
 int x_fits(const pt_plan* p, size_t dyn_bytes) { return (size_t)2 * p->L * p->n * 8 <= dyn_bytes ? 1 : 0; }
 
-template <class R>
 void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
   Work W = carve(p->dwork, p->uwork, p->lay, 0);
   unsigned long long epoch = (++p->launches) << 40;
+  // barrier / abort / rank words start clean on every launch (a watchdog
+  // abort of an earlier launch must not poison this one)
+  *err = cudaMemsetAsync(W.ctl, 0, CTL_WORDS * sizeof(unsigned long long), s);
+  if (*err != cudaSuccess) return;
+  // the max-dynamic-smem attribute belongs to the kernel function, not to the
+  // plan: set this plan's value right before its launch (another live plan
+  // of the same precision may have lowered it since)
+  const void* fn = p->engine == 1 ? kset(p->prec).track_cluster : kset(p->prec).track_grid;
+  *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::max<size_t>(p->engine == 1 ? p->cluster_dyn_smem : p->grid_dyn_smem, 1));
+  if (*err != cudaSuccess) return;
+  pt_step_params spc = sp;
+  TrackIO ioc = io;
   if (p->engine == 1) {
     DevPlan dp = p->dp;
     dp.mgs_smem = p->cluster_dyn_smem > 0;
     dp.mgs_warp = p->cluster_warp;
     dp.bs_smem = stage_fits(p, p->cluster_dyn_smem);
     dp.x_smem = x_fits(p, p->cluster_dyn_smem);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p->cluster_size);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = p->cluster_dyn_smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = p->cluster_size;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    *err = cudaLaunchKernelEx(&cfg, k_track_cluster<R>, dp, W, sp, io, epoch);
+    void* args[] = {&dp, &W, &spc, &ioc, &epoch};
+    *err = launch_ex(fn, p->cluster_size, p->cluster_dyn_smem, s, p->cluster_size, args);
     return;
   }
   DevPlan dp = p->dp;
@@ -660,11 +290,8 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
   dp.mgs_warp = p->grid_warp;
   dp.bs_smem = stage_fits(p, p->grid_dyn_smem);
   dp.x_smem = x_fits(p, p->grid_dyn_smem);
-  pt_step_params spc = sp;
-  TrackIO ioc = io;
   void* args[] = {&dp, &W, &spc, &ioc, &epoch};
-  *err = cudaLaunchCooperativeKernel((const void*)&k_track_grid<R>, dim3(p->grid_blocks), dim3(kThreads), args,
-                                     p->grid_dyn_smem, s);
+  *err = cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, p->grid_dyn_smem, s);
 }
 
 int validate_params(const pt_step_params* sp) {
@@ -804,17 +431,9 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     if (rc) return rc;
     p->d_trace_len = dev_alloc<int>(1, &rc);
     if (rc) return rc;
-    switch (prec) {
-      case PT_D: rc = dispatch_grid_size<double>(p.get(), grid_kernel<double>()); break;
-      case PT_DD: rc = dispatch_grid_size<dd>(p.get(), grid_kernel<dd>()); break;
-      default: rc = dispatch_grid_size<qd>(p.get(), grid_kernel<qd>()); break;
-    }
+    rc = dispatch_grid_size(p.get());
     if (rc) return rc;
-    switch (prec) {
-      case PT_D: rc = setup_cluster<double>(p.get()); break;
-      case PT_DD: rc = setup_cluster<dd>(p.get()); break;
-      default: rc = setup_cluster<qd>(p.get()); break;
-    }
+    rc = setup_cluster(p.get());
     if (rc) return rc;
     *out = p.release();
     return PT_OK;
@@ -882,11 +501,13 @@ int pt_fp64_peak(int device, double* instr_per_s, double* ms_out) {
   cudaEvent_t e0, e1;
   PT_CUDA(cudaEventCreate(&e0));
   PT_CUDA(cudaEventCreate(&e1));
-  k_fp64_peak<<<blocks, threads>>>(d, iters);  // warm-up
+  int it = iters;
+  void* args[] = {&d, &it};
+  PT_CUDA(cudaLaunchKernel(kmisc.fp64_peak, dim3(blocks), dim3(threads), args, 0, 0));  // warm-up
   float best = 1e30f;
   for (int r = 0; r < 5; ++r) {
     PT_CUDA(cudaEventRecord(e0));
-    k_fp64_peak<<<blocks, threads>>>(d, iters);
+    PT_CUDA(cudaLaunchKernel(kmisc.fp64_peak, dim3(blocks), dim3(threads), args, 0, 0));
     PT_CUDA(cudaEventRecord(e1));
     PT_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
@@ -939,20 +560,25 @@ int pt_microbench(int device, int32_t what, double* out) {
   cudaDeviceProp prop;
   PT_CUDA(cudaGetDeviceProperties(&prop, device));
   if (what == 0) {
-    k_latency<<<1, 1>>>(d, 1.25);
+    double seed = 1.25;
+    void* args[] = {&d, &seed};
+    PT_CUDA(cudaLaunchKernel(kmisc.latency, dim3(1), dim3(1), args, 0, 0));
     PT_CUDA(cudaDeviceSynchronize());
-    k_latency<<<1, 1>>>(d, 1.25);
+    PT_CUDA(cudaLaunchKernel(kmisc.latency, dim3(1), dim3(1), args, 0, 0));
   } else if (what == 1) {
     int iters = 2000;
     int blocks = prop.multiProcessorCount;
     void* args[] = {&u, &iters, &d};
-    PT_CUDA(cudaLaunchCooperativeKernel((const void*)&k_barrier, dim3(blocks), dim3(kThreads), args, 0, 0));
+    PT_CUDA(cudaLaunchCooperativeKernel(kmisc.barrier, dim3(blocks), dim3(kThreads), args, 0, 0));
   } else if (what == 2) {
-    k_pingpong<<<prop.multiProcessorCount, 32>>>(u, 10000, d);
+    int iters = 10000;
+    void* args[] = {&u, &iters, &d};
+    PT_CUDA(cudaLaunchKernel(kmisc.pingpong, dim3(prop.multiProcessorCount), dim3(32), args, 0, 0));
   } else if (what == 3) {
-    k_mgs_pieces<<<1, 32>>>(d);
+    void* args[] = {&d};
+    PT_CUDA(cudaLaunchKernel(kmisc.mgs_pieces, dim3(1), dim3(32), args, 0, 0));
     PT_CUDA(cudaDeviceSynchronize());
-    k_mgs_pieces<<<1, 32>>>(d);
+    PT_CUDA(cudaLaunchKernel(kmisc.mgs_pieces, dim3(1), dim3(32), args, 0, 0));
   } else {
     return fail(PT_E_INVAL, "unknown microbenchmark");
   }
@@ -1010,11 +636,7 @@ int pt_track_path_device(pt_plan* p, const double* d_start, const pt_step_params
   cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
   TrackIO io{d_start, d_end, d_stats, p->d_trace, p->trace_cap, p->d_trace_len};
   cudaError_t err = cudaSuccess;
-  switch (p->prec) {
-    case PT_D: launch_grid<double>(p, *sp, io, s, &err); break;
-    case PT_DD: launch_grid<dd>(p, *sp, io, s, &err); break;
-    default: launch_grid<qd>(p, *sp, io, s, &err); break;
-  }
+  launch_grid(p, *sp, io, s, &err);
   if (err != cudaSuccess) return fail(PT_E_CUDA, std::string("track launch: ") + cudaGetErrorString(err));
   return PT_OK;
 }
@@ -1035,9 +657,7 @@ int pt_track_path(pt_plan* p, const double* start, const pt_step_params* sp, dou
 static int ensure_batch(pt_plan* p) {
   if (p->bwork) return PT_OK;
   int per_sm = 0, sms = 0;
-  const void* fn = p->prec == PT_D    ? (const void*)&k_track_batch<double>
-                   : p->prec == PT_DD ? (const void*)&k_track_batch<dd>
-                                      : (const void*)&k_track_batch<qd>;
+  const void* fn = kset(p->prec).track_batch;
   p->batch_dyn_smem = engine_smem(p->L, p->N, p->n, 1, true, &p->batch_warp);
   int rc = set_dyn_smem(fn, p->batch_dyn_smem);
   if (rc) return rc;
@@ -1050,7 +670,7 @@ static int ensure_batch(pt_plan* p) {
   if (rc) return rc;
   p->bu = dev_alloc<unsigned long long>((size_t)p->lay.uslice * p->batch_blocks, &rc);
   if (rc) return rc;
-  p->d_queue = dev_alloc<unsigned long long>(1, &rc);
+  p->d_queue = dev_alloc<unsigned long long>(2, &rc);  // [0] path queue, [1] watchdog abort
   if (rc) return rc;
   PT_CUDA(cudaMemset(p->bwork, 0, (size_t)p->lay.dslice * p->batch_blocks * 8));
   PT_CUDA(cudaMemset(p->bu, 0, (size_t)p->lay.uslice * p->batch_blocks * 8));
@@ -1067,7 +687,9 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   rc = ensure_batch(p);
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
-  PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 8, s));
+  PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 16, s));
+  rc = set_dyn_smem(kset(p->prec).track_batch, p->batch_dyn_smem);  // per-function attribute: this plan's value
+  if (rc) return rc;
   const unsigned long long epoch = (++p->launches) << 40;
   const int blocks = std::min(p->batch_blocks, n_paths);
   DevPlan bdp = p->dp;
@@ -1079,32 +701,12 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   for (int c = 0; c < 6; ++c) bdp.class_beg[c] = p->class_beg_b[c];
   // launched as clusters of one CTA: the warp MGS pushes q_k with st.async,
   // which needs a cluster launch even when the cluster is the CTA itself
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = p->batch_dyn_smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  switch (p->prec) {
-    case PT_D:
-      PT_CUDA(cudaLaunchKernelEx(&cfg, k_track_batch<double>, bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends,
-                                 d_stats, n_paths, p->d_queue, epoch));
-      break;
-    case PT_DD:
-      PT_CUDA(cudaLaunchKernelEx(&cfg, k_track_batch<dd>, bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends,
-                                 d_stats, n_paths, p->d_queue, epoch));
-      break;
-    default:
-      PT_CUDA(cudaLaunchKernelEx(&cfg, k_track_batch<qd>, bdp, p->bwork, p->bu, p->lay, *sp, d_starts, d_ends,
-                                 d_stats, n_paths, p->d_queue, epoch));
-      break;
-  }
+  Layout lay = p->lay;
+  pt_step_params spc = *sp;
+  int np = n_paths;
+  unsigned long long ep = epoch;
+  void* args[] = {&bdp, &p->bwork, &p->bu, &lay, &spc, &d_starts, &d_ends, &d_stats, &np, &p->d_queue, &ep};
+  PT_CUDA(launch_ex(kset(p->prec).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
   PT_CUDA(cudaGetLastError());
   return PT_OK;
 }
@@ -1132,7 +734,11 @@ int pt_track_batch(pt_plan* p, int32_t n_paths, const double* starts, const pt_s
   if (rc) return rc;
   PT_CUDA(cudaMemcpyAsync(ends, p->b_ends, vec * n_paths * 8, cudaMemcpyDeviceToHost, p->stream));
   PT_CUDA(cudaMemcpyAsync(stats, p->b_stats, sizeof(pt_path_stats) * n_paths, cudaMemcpyDeviceToHost, p->stream));
+  unsigned long long abort_flag = 0;
+  PT_CUDA(cudaMemcpyAsync(&abort_flag, p->d_queue + 1, 8, cudaMemcpyDeviceToHost, p->stream));
   PT_CUDA(cudaStreamSynchronize(p->stream));
+  if (abort_flag)
+    return fail(PT_E_TIMEOUT, "device watchdog fired in the batch (paths with failure_kind PT_FAIL_ABORT)");
   return PT_OK;
 }
 
@@ -1153,7 +759,10 @@ int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J
   dp.mgs_smem = 0;
   dp.mgs_warp = 0;
   void* args[] = {&dp, &W, &dx, &t, &dh, &dJ, &dr};
-  const void* fn = p->prec == PT_D ? (const void*)&k_eval<double> : p->prec == PT_DD ? (const void*)&k_eval<dd> : (const void*)&k_eval<qd>;
+  const void* fn = kset(p->prec).eval;
+  rc = set_dyn_smem(fn, p->grid_dyn_smem);
+  if (rc) return rc;
+  PT_CUDA(cudaMemset(W.ctl, 0, CTL_WORDS * sizeof(unsigned long long)));
   PT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, p->grid_dyn_smem, p->stream));
   PT_CUDA(cudaStreamSynchronize(p->stream));
   if (h) PT_CUDA(cudaMemcpy(h, dh, (size_t)2 * L * N * 8, cudaMemcpyDeviceToHost));
@@ -1198,7 +807,7 @@ int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, co
     dp.mgs_gw = ptplan::mgs_group_warps(N);
     const int gpc = kWarps / dp.mgs_gw;
     int per_sm = 0, sms = 0;
-    const void* fn = prec == PT_D ? (const void*)&k_lstsq<double> : prec == PT_DD ? (const void*)&k_lstsq<dd> : (const void*)&k_lstsq<qd>;
+    const void* fn = kset(prec).lstsq;
     rc = occupancy_blocks(fn, device, &per_sm, &sms);
     if (rc) return rc;
     int blocks = std::min(std::min(sms, std::max(1, per_sm) * sms), std::max(1, (n + 1 + gpc - 1) / gpc));
@@ -1252,11 +861,10 @@ int pt_arith_device(int device, pt_prec prec, int32_t op, int64_t count, const d
   PT_CUDA(cudaMemcpy(db, b, bytes, cudaMemcpyHostToDevice));
   PT_CUDA(cudaMemset(dout, 0, bytes));
   const int blocks = (int)std::min<int64_t>(4096, (count + 255) / 256 + 1);
-  switch (prec) {
-    case PT_D: k_arith<double><<<blocks, 256>>>(op, count, da, db, dout); break;
-    case PT_DD: k_arith<dd><<<blocks, 256>>>(op, count, da, db, dout); break;
-    default: k_arith<qd><<<blocks, 256>>>(op, count, da, db, dout); break;
-  }
+  long cnt = (long)count;
+  int opc = op;
+  void* args[] = {&opc, &cnt, &da, &db, &dout};
+  PT_CUDA(cudaLaunchKernel(kset(prec).arith, dim3(blocks), dim3(256), args, 0, 0));
   PT_CUDA(cudaGetLastError());
   PT_CUDA(cudaDeviceSynchronize());
   PT_CUDA(cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost));

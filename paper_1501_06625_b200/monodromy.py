@@ -22,8 +22,8 @@ from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
-from .tracker import (PolynomialSystem, PrecisionMode, StepControlParams, augment_with_linear,
-                      gamma_from_seed, make_homotopy)
+from .systems import (PolynomialSystem, PrecisionMode, StepControlParams, augment_with_linear,
+                      gamma_from_seed)
 
 # (g, f, gamma, starts[P,2,L,n], params) -> (ends[P,2,L,n], success[P])
 BatchTracker = Callable[[PolynomialSystem, PolynomialSystem, np.ndarray, np.ndarray, StepControlParams],
@@ -34,6 +34,7 @@ def gpu_batch_tracker(device: int = 0) -> BatchTracker:
     """The product path: one plan per leg, all points in one batch launch."""
 
     def run(g, f, gamma, starts, params):
+        from .tracker import make_homotopy
         hom = make_homotopy(g, f, gamma, 1, device=device)
         ends, outs = hom.track_batch(starts, params)
         return ends, np.array([o.success for o in outs], dtype=bool)

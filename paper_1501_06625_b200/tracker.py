@@ -29,200 +29,23 @@ import numpy as np
 from . import _native as nat
 
 
-class PrecisionMode(enum.IntEnum):  # multiprec.hpp:27
-    D = 0
-    DD = 1
-    QD = 2
-
-    @property
-    def limbs(self) -> int:
-        return (1, 2, 4)[int(self)]
-
-    @staticmethod
-    def parse(text: str) -> "PrecisionMode":  # precision.cpp:22-27
-        m = {"d": PrecisionMode.D, "dd": PrecisionMode.DD, "qd": PrecisionMode.QD}
-        if text not in m:
-            raise ValueError(f"unknown precision mode '{text}' (expected d, dd, or qd)")
-        return m[text]
-
-
-def limbs_from_complex(z, prec: PrecisionMode) -> np.ndarray:
-    """complex128 vector -> (2, L, n) limbs with the value in limb 0."""
-    z = np.asarray(z, dtype=np.complex128).reshape(-1)
-    out = np.zeros((2, prec.limbs, z.size))
-    out[0, 0] = z.real
-    out[1, 0] = z.imag
-    return out
+from .systems import (  # noqa: F401  (re-exported: the SPEC names live here too)
+    PolynomialSystem,
+    PrecisionMode,
+    StepControlParams,
+    augment_with_linear,
+    chandrasekhar,
+    complex_from_limbs,
+    cyclic_system,
+    gamma_from_seed,
+    limbs_from_complex,
+    random_dense,
+    total_degree_start,
+    unit_complex,
+)
 
 
-def complex_from_limbs(a: np.ndarray) -> np.ndarray:
-    """(2, L, n) limbs -> complex128 (sum of limbs rounded to binary64)."""
-    a = np.asarray(a)
-    return a[0].sum(axis=0) + 1j * a[1].sum(axis=0)
-
-
-@dataclass
-class PolynomialSystem:
-    """Canonical distributed form, pt_system_desc layout."""
-
-    n_vars: int
-    eq_ptr: np.ndarray
-    term_ptr: np.ndarray
-    var: np.ndarray
-    exp: np.ndarray
-    coef: np.ndarray  # (2, L, n_terms)
-    prec: PrecisionMode
-
-    @property
-    def n_eqs(self) -> int:
-        return int(self.eq_ptr.size - 1)
-
-    @property
-    def n_terms(self) -> int:
-        return int(self.term_ptr.size - 1)
-
-    def desc(self) -> nat.SystemDesc:
-        for name in ("eq_ptr", "term_ptr", "var", "exp"):
-            setattr(self, name, np.ascontiguousarray(getattr(self, name), dtype=np.int32))
-        self.coef = np.ascontiguousarray(self.coef, dtype=np.float64)
-        d = nat.SystemDesc()
-        d.n_vars, d.n_eqs, d.n_terms = self.n_vars, self.n_eqs, self.n_terms
-        d.eq_ptr = nat.iptr(self.eq_ptr)
-        d.term_ptr = nat.iptr(self.term_ptr)
-        d.var = nat.iptr(self.var if self.var.size else np.zeros(1, np.int32))
-        d.exp = nat.iptr(self.exp if self.exp.size else np.ones(1, np.int32))
-        d.coef = nat.dptr(self.coef)
-        return d
-
-    def terms(self, i: int):
-        """(support [(var, exp)], complex128 coefficient) of equation i."""
-        out = []
-        for t in range(self.eq_ptr[i], self.eq_ptr[i + 1]):
-            sup = [(int(self.var[q]), int(self.exp[q])) for q in range(self.term_ptr[t], self.term_ptr[t + 1])]
-            c = self.coef[0, :, t].sum() + 1j * self.coef[1, :, t].sum()
-            out.append((sup, c))
-        return out
-
-    @staticmethod
-    def _from_sysbuf(buf, prec: PrecisionMode) -> "PolynomialSystem":
-        d = nat.SystemDesc()
-        nat.check(nat.lib.pt_sysbuf_desc(buf, C.byref(d)))
-        T = d.n_terms
-        V = d.term_ptr[T] if T > 0 else 0
-        arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy() if n > 0 else np.zeros(0, np.int32)
-        sysm = PolynomialSystem(
-            n_vars=d.n_vars,
-            eq_ptr=arr(d.eq_ptr, d.n_eqs + 1),
-            term_ptr=arr(d.term_ptr, T + 1),
-            var=arr(d.var, V),
-            exp=arr(d.exp, V),
-            coef=np.ctypeslib.as_array(d.coef, shape=(2 * prec.limbs * max(T, 1),)).copy()[: 2 * prec.limbs * T]
-            .reshape(2, prec.limbs, T),
-            prec=prec,
-        )
-        nat.lib.pt_sysbuf_free(buf)
-        return sysm
-
-    @staticmethod
-    def from_terms(n_vars: int, equations, prec: PrecisionMode) -> "PolynomialSystem":
-        """Build from [[(support, coef), ...], ...] with support [(var, exp), ...]
-        (var ascending, exp >= 1) and coef a complex number or a (2, L) limb
-        array.  Term order is kept as given."""
-        L = prec.limbs
-        eq_ptr, term_ptr, var, exp, coefs = [0], [0], [], [], []
-        for eq in equations:
-            for sup, c in eq:
-                for v, e in sup:
-                    var.append(v)
-                    exp.append(e)
-                term_ptr.append(len(var))
-                cl = np.zeros((2, L))
-                if np.ndim(c) == 0:
-                    cl[0, 0], cl[1, 0] = complex(c).real, complex(c).imag
-                else:
-                    cl[:] = np.asarray(c, dtype=np.float64).reshape(2, L)
-                coefs.append(cl)
-            eq_ptr.append(len(term_ptr) - 1)
-        coef = np.stack(coefs, axis=-1) if coefs else np.zeros((2, L, 0))
-        return PolynomialSystem(n_vars, np.array(eq_ptr, np.int32), np.array(term_ptr, np.int32),
-                                np.array(var, np.int32), np.array(exp, np.int32), coef, prec)
-
-
-def _gen(fn, *args, prec: PrecisionMode) -> PolynomialSystem:
-    buf = C.c_void_p()
-    nat.check(fn(*args, int(prec), C.byref(buf)))
-    return PolynomialSystem._from_sysbuf(buf, prec)
-
-
-def cyclic_system(n: int, prec: PrecisionMode = PrecisionMode.DD) -> PolynomialSystem:
-    """Cyclic n-roots, Eq. (5)."""
-    return _gen(nat.lib.pt_gen_cyclic, n, prec=prec)
-
-
-def augment_with_linear(n_cyclic: int, dim: int, seed: int,
-                        prec: PrecisionMode = PrecisionMode.DD) -> PolynomialSystem:
-    """cyclic-n plus `dim` random affine slices, Eq. (6)."""
-    fb = C.c_void_p()
-    nat.check(nat.lib.pt_gen_cyclic(n_cyclic, int(prec), C.byref(fb)))
-    out = C.c_void_p()
-    rc = nat.lib.pt_gen_augment(fb, dim, C.c_uint64(seed), int(prec), C.byref(out))
-    nat.lib.pt_sysbuf_free(fb)
-    nat.check(rc)
-    return PolynomialSystem._from_sysbuf(out, prec)
-
-
-def chandrasekhar(n: int, c: float = 0.51234, prec: PrecisionMode = PrecisionMode.DD) -> PolynomialSystem:
-    """Discretised Chandrasekhar H-equation (BASELINE config 2)."""
-    return _gen(nat.lib.pt_gen_chandra, n, C.c_double(c), prec=prec)
-
-
-def random_dense(n: int, degree: int, n_monomials: int, seed: int,
-                 prec: PrecisionMode = PrecisionMode.DD) -> PolynomialSystem:
-    """n equations on one shared random support (BASELINE configs 3 and 5)."""
-    return _gen(nat.lib.pt_gen_random_dense, n, degree, n_monomials, C.c_uint64(seed), prec=prec)
-
-
-def total_degree_start(n: int, degree: int, prec: PrecisionMode = PrecisionMode.DD) -> PolynomialSystem:
-    """g_i = x_i^degree - 1."""
-    return _gen(nat.lib.pt_gen_total_degree, n, degree, prec=prec)
-
-
-def gamma_from_seed(seed: int, prec: PrecisionMode) -> np.ndarray:
-    """Rng(seed).unit<R>() (rng.hpp:38-41) as 2L limbs."""
-    out = np.zeros(2 * prec.limbs)
-    nat.check(nat.lib.pt_gen_gamma(C.c_uint64(seed), int(prec), nat.dptr(out)))
-    return out
-
-
-def unit_complex(theta: float, prec: PrecisionMode) -> np.ndarray:
-    """unit_complex<R>(theta) (complex.hpp:141-148) as 2L limbs."""
-    out = np.zeros(2 * prec.limbs)
-    nat.check(nat.lib.pt_gen_unit_complex(C.c_double(theta), int(prec), nat.dptr(out)))
-    return out
-
-
-@dataclass
-class StepControlParams:  # SPEC.md:448-451 + NewtonParams SPEC.md:357-359
-    max_step: float = 0.1
-    min_step: float = 1e-6
-    max_steps: int = 500
-    pred_degree: int = 4
-    newton_max_iter: int = 6
-    newton_tol: float = 1e-20
-
-    @staticmethod
-    def defaults(prec: PrecisionMode) -> "StepControlParams":
-        sp = nat.StepParams()
-        nat.check(nat.lib.pt_default_params(int(prec), C.byref(sp)))
-        return StepControlParams(sp.max_step, sp.min_step, sp.max_steps, sp.pred_degree, sp.newton_max_iter,
-                                 sp.newton_tol)
-
-    def native(self) -> nat.StepParams:
-        return nat.StepParams(self.max_step, self.min_step, self.max_steps, self.pred_degree,
-                              self.newton_max_iter, 0, self.newton_tol)
-
-
-FAILURE_KINDS = {0: "none", 1: "start", 2: "max-steps", 3: "min-step"}
+FAILURE_KINDS = {0: "none", 1: "start", 2: "max-steps", 3: "min-step", 4: "abort"}
 
 
 @dataclass

@@ -20,7 +20,7 @@ from typing import Optional
 
 import numpy as np
 
-from .tracker import (
+from .systems import (
     PolynomialSystem,
     PrecisionMode,
     StepControlParams,

@@ -17,23 +17,47 @@ from paper_1501_06625_b200 import workloads as W
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_functions():
-    names = set()
-    for fn in os.listdir(os.path.join(ROOT, "include")):
-        if fn.endswith(".h"):
-            text = open(os.path.join(ROOT, "include", fn)).read()
-            text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-            names |= set(re.findall(r"\b(pt_\w+)\s*\(", text))
-    return names
+def declared_functions(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(pt_\w+)\s*\(", text))
 
 
 def test_every_declared_symbol_is_exported():
-    names = declared_functions()
-    assert len(names) >= 25
-    lib = C.CDLL(nat.LIB_PATH)
-    missing = [n for n in sorted(names) if not hasattr(lib, n)]
-    assert not missing, missing
-    assert set(nat.PROTOTYPES) == names, set(nat.PROTOTYPES) ^ names
+    """Each header's functions are exported by its library, and the ctypes
+    prototype tables cover exactly the declarations."""
+    from paper_1501_06625_b200 import _inputs as inp
+    for header, mod, at_least in (("pathtrack_b200.h", nat, 24), ("pathtrack_inputs.h", inp, 25)):
+        names = declared_functions(header)
+        assert len(names) >= at_least
+        lib = C.CDLL(mod.LIB_PATH)
+        missing = [n for n in sorted(names) if not hasattr(lib, n)]
+        assert not missing, (header, missing)
+        assert set(mod.PROTOTYPES) == names, (header, set(mod.PROTOTYPES) ^ names)
+
+
+def test_inputs_never_load_the_tracker_library():
+    """Workload construction (what the reference arm of bench.py and the
+    oracle tests use) maps libpt_inputs.so only, never libpathtrack_b200.so."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1501_06625_b200 import workloads as W, PrecisionMode as PM\n"
+            "w = W.chandra(8, PM.DD); W.batch(n_paths=4); W.cyclic_leg(4, PM.DD)\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "print('inputs' if 'libpt_inputs.so' in maps else 'no-inputs',"
+            " 'TRACKER' if 'libpathtrack_b200.so' in maps else 'clean')\n") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True).stdout.split()
+    assert out == ["inputs", "clean"], out
+
+
+def test_default_params_match_the_library():
+    for prec in PM:
+        sp = nat.StepParams()
+        nat.check(nat.lib.pt_default_params(int(prec), C.byref(sp)))
+        py = pt.StepControlParams.defaults(prec)
+        assert (sp.max_step, sp.min_step, sp.max_steps, sp.pred_degree, sp.newton_max_iter, sp.newton_tol) == (
+            py.max_step, py.min_step, py.max_steps, py.pred_degree, py.newton_max_iter, py.newton_tol)
 
 
 def test_struct_layouts_match_header():

@@ -33,3 +33,12 @@ def test_cpp_adapter_on_reference_headers(tmp_path):
 def test_cpp_adapter_on_restated_headers(tmp_path):
     r = _build_and_run(tmp_path, False)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_adapter_tracks_on_device(tmp_path, gpu):
+    """The C++ adapter's device path: plan, track_path through the C-ABI,
+    end point x = 2 of the SPEC.md:472 homotopy (restated headers: the box
+    has no /root/reference)."""
+    r = _build_and_run(tmp_path, os.path.isdir(REF_INC))
+    assert r.returncode == 0 and "device: success=1" in r.stdout, r.stdout + r.stderr
