@@ -73,6 +73,11 @@ class Oracle:
                                           C.c_double, _dp, _dp, _dp]
         lib.orc_lstsq.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
         lib.orc_arith.argtypes = [C.c_int, C.c_int, C.c_long, _dp, _dp, _dp]
+        lib.orc_track_batch.argtypes = [C.c_int, C.POINTER(SystemDesc), C.POINTER(SystemDesc), _dp, C.c_int, C.c_int,
+                                        _dp, C.POINTER(StepParams), _dp, C.POINTER(PathStats), C.c_int]
+        if variant == "reference":
+            lib.orc_ref_hex_limbs.argtypes = [_dp, C.c_int, C.c_char_p, C.c_int]
+            lib.orc_ref_parse_hex_limbs.argtypes = [C.c_char_p, C.c_int, _dp, C.c_int, C.POINTER(C.c_int)]
         lib.orc_set_threads.argtypes = [C.c_int]
         lib.orc_variant.restype = C.c_char_p
         lib.orc_last_error.restype = C.c_char_p
@@ -115,6 +120,39 @@ class Oracle:
                                             start.ctypes.data_as(_dp), C.byref(sp), end.ctypes.data_as(_dp),
                                             C.byref(st), tr if trace_cap else None, trace_cap, C.byref(tl)))
         return end, st, list(tr[: min(tl.value, trace_cap)]) if trace_cap else []
+
+    def track_batch(self, prec: int, g, f, gamma, k, starts, params, threads: int):
+        """Independent paths on a pool of `threads` host threads, one
+        single-threaded tracker per path (the batch CPU baseline)."""
+        gd, kg = self._desc(g)
+        fd, kf = self._desc(f)
+        gamma = np.ascontiguousarray(gamma, dtype=np.float64)
+        starts = np.ascontiguousarray(starts, dtype=np.float64)
+        P = starts.shape[0]
+        ends = np.zeros_like(starts)
+        stats = (PathStats * max(P, 1))()
+        sp = StepParams(params.max_step, params.min_step, params.max_steps, params.pred_degree,
+                        params.newton_max_iter, 0, params.newton_tol)
+        self._check(self.lib.orc_track_batch(int(prec), C.byref(gd), C.byref(fd), gamma.ctypes.data_as(_dp), int(k),
+                                             P, starts.ctypes.data_as(_dp), C.byref(sp), ends.ctypes.data_as(_dp),
+                                             stats, int(threads)))
+        return ends, list(stats[:P])
+
+    def ref_hex_limbs(self, limbs) -> str:
+        """The reference's hex_limbs (hexio.cpp) -- reference variant only."""
+        a = np.ascontiguousarray(np.atleast_1d(limbs), dtype=np.float64)
+        buf = C.create_string_buffer(32 + 17 * a.size)
+        self._check(self.lib.orc_ref_hex_limbs(a.ctypes.data_as(_dp), a.size, buf, len(buf)))
+        return buf.value.decode()
+
+    def ref_parse_hex_limbs(self, text: str):
+        """The reference's parse_hex_limbs; None when it throws."""
+        raw = text.encode()
+        out = np.zeros(64)
+        cnt = C.c_int()
+        if self.lib.orc_ref_parse_hex_limbs(raw, len(raw), out.ctypes.data_as(_dp), 64, C.byref(cnt)) != 0:
+            return None
+        return out[: cnt.value].copy()
 
     def eval_homotopy(self, prec: int, g, f, gamma, k, x, t):
         gd, kg = self._desc(g)

@@ -10,8 +10,14 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <atomic>
+#include <thread>
+#include <vector>
 
 #include "orc_tracker.hpp"
+#ifdef ORC_USE_REFERENCE
+#include "pathtrack/hexio.hpp"
+#endif
 
 using namespace orc_track;
 
@@ -134,9 +140,74 @@ int guarded(F&& f) {
   }
 }
 
+// Batch baseline: a pool of `threads` host threads
+// over independent paths (one tracker per path), each tracker
+// single-threaded inside (its OpenMP regions run on 1 thread).
+template <class R>
+int run_batch(const SystemDesc* g, const SystemDesc* f, const double* gamma, int k, int n_paths,
+              const double* starts, const StepParams* P, double* ends, PathStats* st, int threads) {
+  std::atomic<int> next{0};
+  std::atomic<int> bad{0};
+  auto worker = [&]() {
+#ifdef _OPENMP
+    omp_set_num_threads(1);
+#endif
+    try {
+      Tracker<R> T;
+      T.build(*g, *f, gamma, k);
+      const long PS = 2L * Tracker<R>::L * T.n;
+      std::vector<typename Tracker<R>::C> x0(T.n), x1;
+      for (int p = next++; p < n_paths; p = next++) {
+        for (int i = 0; i < T.n; ++i) x0[i] = Tracker<R>::load_c(starts + p * PS, T.n, i);
+        T.track(x0, *P, x1, st[p], nullptr);
+        for (int i = 0; i < T.n; ++i) Tracker<R>::store_c(ends + p * PS, T.n, i, x1[i]);
+      }
+    } catch (...) {
+      bad = 1;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < (threads > 0 ? threads : 1); ++t) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  return bad ? -1 : 0;
+}
+
 }  // namespace
 
 extern "C" {
+
+int orc_track_batch(int prec, const SystemDesc* g, const SystemDesc* f, const double* gamma, int k, int n_paths,
+                    const double* starts, const StepParams* P, double* ends, PathStats* st, int threads) {
+  return guarded([&] {
+    switch (prec) {
+      case 0: return run_batch<double>(g, f, gamma, k, n_paths, starts, P, ends, st, threads);
+      case 1: return run_batch<A::DoubleDouble>(g, f, gamma, k, n_paths, starts, P, ends, st, threads);
+      case 2: return run_batch<A::QuadDouble>(g, f, gamma, k, n_paths, starts, P, ends, st, threads);
+    }
+    return -1;
+  });
+}
+
+#ifdef ORC_USE_REFERENCE
+// The reference's own hex I/O (proj/src/hexio.cpp), for pinning the product's
+// restatement (libpt_inputs.so).  Exceptions become -1 + orc_last_error().
+int orc_ref_hex_limbs(const double* limbs, int count, char* out, int cap) {
+  return guarded([&] {
+    const std::string s = pathtrack::hex_limbs(std::span<const double>(limbs, (size_t)count));
+    if ((int)s.size() + 1 > cap) throw std::invalid_argument("output buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  });
+}
+int orc_ref_parse_hex_limbs(const char* text, int len, double* out, int cap, int* count) {
+  return guarded([&] {
+    const std::vector<double> v = pathtrack::parse_hex_limbs(std::string_view(text, (size_t)len));
+    *count = (int)v.size();
+    for (int i = 0; i < (int)v.size() && i < cap; ++i) out[i] = v[i];
+    return 0;
+  });
+}
+#endif
 
 const char* orc_variant(void) {
 #ifdef ORC_USE_REFERENCE
