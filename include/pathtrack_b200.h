@@ -199,6 +199,11 @@ int pt_track_batch_device(pt_plan* plan, int32_t n_paths, const double* d_starts
  * column-major), *rmax = max_modulus(h).  Any output may be NULL. */
 int pt_eval_homotopy(pt_plan* plan, const double* x, double t, double* h, double* J, double* rmax);
 
+/* run_evalbench: device time of one evaluation and
+ * differentiation pass (h and J into the plan's workspace) at (x, t),
+ * averaged over `reps` back-to-back launches after one warm-up. */
+int pt_eval_bench(pt_plan* plan, const double* x, double t, int32_t reps, double* ms_per_eval);
+
 /* least_squares_solve by MGS on the device: A (N x n, column-major), b (N). */
 int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, const double* b, double* x);
 

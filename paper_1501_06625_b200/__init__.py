@@ -38,7 +38,7 @@ from .systems import (  # noqa: F401
 
 __version__ = "0.2.0"
 
-_TRACKER_NAMES = {"FAILURE_KINDS", "Homotopy", "TrackOutcome", "arith", "device_count", "least_squares_solve",
+_TRACKER_NAMES = {"FAILURE_KINDS", "Homotopy", "TrackOutcome", "arith", "device_count", "eval_bench", "least_squares_solve",
                   "make_homotopy"}
 _SUBMODULES = {"monodromy", "workloads", "pieri", "multi", "cli", "tracker"}
 

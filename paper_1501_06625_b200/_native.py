@@ -39,6 +39,7 @@ PROTOTYPES = {
     "pt_track_batch": (C.c_int, [_vp, C.c_int32, _dp, C.POINTER(StepParams), _dp, C.POINTER(PathStats)]),
     "pt_track_batch_device": (C.c_int, [_vp, C.c_int32, _vp, C.POINTER(StepParams), _vp, _vp, _vp]),
     "pt_eval_homotopy": (C.c_int, [_vp, _dp, C.c_double, _dp, _dp, _dp]),
+    "pt_eval_bench": (C.c_int, [_vp, _dp, C.c_double, C.c_int32, _dp]),
     "pt_lstsq": (C.c_int, [C.c_int, C.c_int, C.c_int32, C.c_int32, _dp, _dp, _dp]),
     "pt_arith_device": (C.c_int, [C.c_int, C.c_int, C.c_int32, C.c_int64, _dp, _dp, _dp]),
     "pt_arith_host": (C.c_int, [C.c_int, C.c_int32, C.c_int64, _dp, _dp, _dp]),

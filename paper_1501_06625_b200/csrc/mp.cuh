@@ -242,21 +242,28 @@ PT_HD double r_limb(double a, int) { return a; }
 PT_HD void r_set_limb(double& a, int, double v) { a = v; }
 
 // ----- double-double (multiprec.hpp:91-189) -----
-// multiprec.hpp:102-107 returns {h, 0} for a non-finite h.  On the device
-// that select is dropped by default: quick_two_sum of a non-finite h gives
-// {h (or NaN), NaN}, so only the LOW limb of a non-finite value differs
-// (NaN instead of 0) and every finite result is bit-identical.  The select --
-// a predicate or mask per DD operation -- made ptxas serialise independent DD
-// chains on the MGS critical path (tools/mgs_bench.cu: complex DD axpy of
-// two rows 1.4k -> 0.55k cycles, warp tree 1.8k -> 1.1k, per MGS column
-// 3.9 -> 2.9 us).  Non-finite values only occur on paths that fail; NaN
-// payloads differ between the GPU and x86 anyway.  -DPT_DD_EXACT_NONFINITE
-// restores the reference's branch on the device.
+// multiprec.hpp:102-107 returns {h, 0} for a non-finite h; the device does
+// the same with integer masks (dd_norm below), so non-finite DD values match
+// the reference too (NaN payloads aside: the GPU's FP64 units produce the
+// canonical NaN, x86 propagates the operand's payload).
+// -DPT_DD_FAST_NONFINITE drops the non-finite fix-up (round-1 behaviour).
 PT_HD dd dd_norm(double h, double l) {  // multiprec.hpp:102-107
   double e;
   double s = quick_two_sum(h, l, e);
-#if defined(__CUDA_ARCH__) && !defined(PT_DD_EXACT_NONFINITE)
+#if defined(__CUDA_ARCH__) && defined(PT_DD_FAST_NONFINITE)
   return {s, e};
+#elif defined(__CUDA_ARCH__)
+  // {h, 0} for a non-finite h, branch- and predicate-free: an all-ones mask
+  // from h's exponent field on the integer pipe (it depends on h only, so
+  // it is ready long before s and e), then AND / AND-OR on the bit patterns.
+  // A predicated select here made ptxas serialise independent DD chains
+  // (round 1); the mask form keeps them interleaved and is bit-identical to
+  // the reference, non-finite values included.
+  const unsigned hw = (unsigned)__double2hiint(h);
+  const int t = (int)((hw & 0x7ff00000u) - 0x7ff00000u);          // 0 iff h is inf / NaN
+  const long long m = (long long)((t | -t) >> 31);                  // all ones iff h is finite
+  const long long sb = __double_as_longlong(s), hb = __double_as_longlong(h);
+  return {__longlong_as_double((sb & m) | (hb & ~m)), __longlong_as_double(__double_as_longlong(e) & m)};
 #else
   if (!finite(h)) return {h, 0.0};
   return {s, e};

@@ -775,6 +775,45 @@ int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J
   return read_abort(p, W.ctl);
 }
 
+int pt_eval_bench(pt_plan* p, const double* x, double t, int32_t reps, double* ms_per_eval) {
+  if (!p || !x || reps < 1 || !ms_per_eval) return fail(PT_E_INVAL, "bad eval-bench arguments");
+  PT_CUDA(cudaSetDevice(p->device));
+  const int L = p->L, n = p->n;
+  int rc = 0;
+  double* dx = dev_alloc<double>((size_t)2 * L * n, &rc);
+  if (rc) return rc;
+  std::unique_ptr<double, decltype(&cudaFree)> gx(dx, &cudaFree);
+  PT_CUDA(cudaMemcpy(dx, x, (size_t)2 * L * n * 8, cudaMemcpyHostToDevice));
+  Work W = carve(p->dwork, p->uwork, p->lay, 0);
+  DevPlan dp = p->dp;
+  dp.mgs_smem = 0;
+  dp.mgs_warp = 0;
+  double* null = nullptr;
+  void* args[] = {&dp, &W, &dx, &t, &null, &null, &null};
+  const void* fn = kset(p->prec).eval;
+  rc = set_dyn_smem(fn, p->grid_dyn_smem);
+  if (rc) return rc;
+  PT_CUDA(cudaMemset(W.ctl, 0, CTL_WORDS * sizeof(unsigned long long)));
+  cudaEvent_t e0, e1;
+  PT_CUDA(cudaEventCreate(&e0));
+  PT_CUDA(cudaEventCreate(&e1));
+  // one untimed warm-up pass, then `reps` passes between events on the plan's stream
+  cudaError_t err = cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, p->grid_dyn_smem,
+                                                p->stream);
+  if (err == cudaSuccess) err = cudaEventRecord(e0, p->stream);
+  for (int r = 0; r < reps && err == cudaSuccess; ++r)
+    err = cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, p->grid_dyn_smem, p->stream);
+  if (err == cudaSuccess) err = cudaEventRecord(e1, p->stream);
+  if (err == cudaSuccess) err = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (err != cudaSuccess) return fail(PT_E_CUDA, std::string("eval bench: ") + cudaGetErrorString(err));
+  *ms_per_eval = ms / reps;
+  return read_abort(p, W.ctl);
+}
+
 int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, const double* b, double* x) {
   return guarded([&]() -> int {
     if (!A || !b || !x || n < 1 || N < n || n > kMaxRowsPerThread * kThreads || N > kMaxElems * 256)

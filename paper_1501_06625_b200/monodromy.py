@@ -28,6 +28,11 @@ from .systems import (PolynomialSystem, PrecisionMode, StepControlParams, augmen
 # (g, f, gamma, starts[P,2,L,n], params) -> (ends[P,2,L,n], success[P])
 BatchTracker = Callable[[PolynomialSystem, PolynomialSystem, np.ndarray, np.ndarray, StepControlParams],
                         tuple]
+# (system, points[P,2,L,n]) -> max_i |f_i(point)| per point (binary64), evaluated in the system's precision
+Evaluator = Callable[[PolynomialSystem, np.ndarray], np.ndarray]
+
+# point-matching tolerance per precision (SPEC.md "DESIGN DECISIONS": 1e-6 D, 1e-12 DD)
+MATCH_TOL = {PrecisionMode.D: 1e-6, PrecisionMode.DD: 1e-12, PrecisionMode.QD: 1e-12}
 
 
 def gpu_batch_tracker(device: int = 0) -> BatchTracker:
@@ -38,6 +43,21 @@ def gpu_batch_tracker(device: int = 0) -> BatchTracker:
         hom = make_homotopy(g, f, gamma, 1, device=device)
         ends, outs = hom.track_batch(starts, params)
         return ends, np.array([o.success for o in outs], dtype=bool)
+
+    return run
+
+
+def gpu_evaluator(device: int = 0) -> Evaluator:
+    """max_modulus(f(x)) on the device: evaluate_homotopy of (f, f) at t = 1."""
+
+    def run(sysm, points):
+        from .tracker import make_homotopy
+        one = np.zeros(2 * sysm.prec.limbs)
+        one[0] = 1.0
+        hom = make_homotopy(sysm, sysm, one, 1, device=device)
+        out = np.array([hom.evaluate(p, 1.0)[2] for p in points])
+        hom.close()
+        return out
 
     return run
 
@@ -80,6 +100,10 @@ class WitnessSet:
     points: List[np.ndarray] = field(default_factory=list)   # each [2, L, n]
     loops: int = 0
     failed_paths: int = 0
+    residuals: List[float] = field(default_factory=list)     # (f, L) residual of each stored point
+    rejected_residual: int = 0   # endpoints whose (f, L) residual failed the insertion check
+    jumped: int = 0              # endpoints that left the start component (path jumping)
+    log: List[str] = field(default_factory=list)             # loop-by-loop discoveries
 
     @property
     def degree(self) -> int:
@@ -88,21 +112,37 @@ class WitnessSet:
 
 def monodromy_degree(n_cyclic: int, dim: int, start_witness: Sequence[np.ndarray], seed: int,
                      stabilization_loops: int, prec: PrecisionMode = PrecisionMode.DD,
-                     loop_budget: int = 64, slice_seed: int = 1, match_tol: float = 1e-6,
+                     loop_budget: int = 64, slice_seed: int = 1, match_tol: Optional[float] = None,
                      params: Optional[StepControlParams] = None,
-                     tracker: Optional[BatchTracker] = None) -> WitnessSet:
+                     tracker: Optional[BatchTracker] = None,
+                     evaluator: Optional[Evaluator] = None, residual_tol: Optional[float] = None,
+                     component_key: Optional[Callable[[np.ndarray], complex]] = None) -> WitnessSet:
     """monodromy_degree on the cyclic-n component cut by
     `dim` affine slices L (augment_with_linear(n, dim, slice_seed)): every loop
     sends all known points around a fresh (alpha, beta, K) loop and adds the
-    endpoints at distance > match_tol from every known point; stops after
-    `stabilization_loops` consecutive loops without a new point, or after
-    `loop_budget` loops.  Raises RuntimeError when every path of every loop fails."""
+    endpoints at distance > match_tol (default MATCH_TOL[prec]) from every
+    known point; stops after `stabilization_loops` consecutive loops without a
+    new point, or after `loop_budget` loops.  Raises RuntimeError when every
+    path of every loop fails.
+
+    Insertion checks (SPEC.md bench invariants): the (f, L) residual of a new
+    point is re-evaluated (`evaluator`, default the device) and must be below
+    `residual_tol` (default the corrector tolerance); with `component_key`
+    (an invariant of the start component, e.g. workloads.backelin_component_key)
+    an endpoint whose key differs from the start witness's has jumped to
+    another component -- a path-crossing failure of that loop -- and is
+    rejected, not counted."""
     if not start_witness:
         raise ValueError("start witness set is empty")
     params = params or StepControlParams.defaults(prec)
     tracker = tracker or gpu_batch_tracker()
+    evaluator = evaluator or gpu_evaluator()
+    match_tol = MATCH_TOL[prec] if match_tol is None else match_tol
+    residual_tol = params.newton_tol if residual_tol is None else residual_tol
     fL = augment_with_linear(n_cyclic, dim, slice_seed, prec)
     ws = WitnessSet([np.array(p, dtype=np.float64) for p in start_witness])
+    ws.residuals = [float(r) for r in evaluator(fL, np.stack(ws.points))]
+    key0 = component_key(ws.points[0]) if component_key else None
     quiet, any_ok = 0, False
     while quiet < stabilization_loops and ws.loops < loop_budget:
         k_seed, a_seed, b_seed = loop_seeds(seed, ws.loops)
@@ -112,11 +152,23 @@ def monodromy_degree(n_cyclic: int, dim: int, start_witness: Sequence[np.ndarray
         ws.loops += 1
         ws.failed_paths += int(np.count_nonzero(~res.success))
         any_ok |= bool(res.success.any())
+        cand = [np.array(p) for p, ok in zip(res.points, res.success)
+                if ok and all(_distinct(p, q, match_tol) for q in ws.points)]
+        if key0 is not None:
+            kept = [p for p in cand if abs(component_key(p) - key0) <= 1e-6 * max(1.0, abs(key0))]
+            ws.jumped += len(cand) - len(kept)
+            cand = kept
         new = 0
-        for p, ok in zip(res.points, res.success):
-            if ok and all(_distinct(p, q, match_tol) for q in ws.points):
-                ws.points.append(np.array(p))
-                new += 1
+        if cand:
+            resid = evaluator(fL, np.stack(cand))
+            for p, r in zip(cand, resid):
+                if not (r < residual_tol):
+                    ws.rejected_residual += 1
+                elif all(_distinct(p, q, match_tol) for q in ws.points):
+                    ws.points.append(p)
+                    ws.residuals.append(float(r))
+                    new += 1
+        ws.log.append(f"loop {ws.loops}: {new} new, degree {ws.degree}")
         quiet = 0 if new else quiet + 1
     if ws.loops and not any_ok:
         raise RuntimeError(f"monodromy: all {ws.failed_paths} paths of {ws.loops} loops failed")

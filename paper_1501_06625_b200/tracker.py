@@ -158,6 +158,14 @@ class Homotopy:
         return h, J, float(r[0])
 
 
+def eval_bench(hom: Homotopy, x: np.ndarray, t: float, reps: int) -> float:
+    """Device milliseconds per evaluation + differentiation pass (pt_eval_bench)."""
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(2, hom.prec.limbs, hom.n)
+    ms = np.zeros(1)
+    nat.check(nat.lib.pt_eval_bench(hom.plan, nat.dptr(x), C.c_double(t), int(reps), nat.dptr(ms)))
+    return float(ms[0])
+
+
 def make_homotopy(g: PolynomialSystem, f: PolynomialSystem, gamma: np.ndarray, k: int = 2,
                   device: int = 0) -> Homotopy:
     return Homotopy(g, f, gamma, k, device)

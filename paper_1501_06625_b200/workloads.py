@@ -91,6 +91,49 @@ def backelin_witness(aug: PolynomialSystem, m: int, dim: int) -> np.ndarray:
     return x
 
 
+def backelin_component_key(m: int):
+    """Invariant of a Backelin component of cyclic-(m^2): on the family
+    x_{a m + b} = omega^a r_b the product r_0 ... r_{m-1} = x_0 ... x_{m-1} is
+    an m-th root of unity fixed along the component (prod x = (prod r)^m = 1
+    splits the family into m components {prod r = zeta}); a monodromy endpoint
+    with a different value has jumped to another component."""
+
+    def key(point: np.ndarray) -> complex:
+        z = point[0].sum(axis=0)[:m] + 1j * point[1].sum(axis=0)[:m]
+        return complex(np.prod(z))
+
+    return key
+
+
+def cyclic4_witness(slice_row: np.ndarray, family: int = 1) -> list:
+    """cyclic4_witness: family 1 (a, 1/a, -a, -1/a) or
+    family 2 (a, -1/a, -a, 1/a) substituted into the affine slice
+    c_0 + c_1 x_0 + ... + c_4 x_3 = 0 gives (c_1 - c_3 s) a^2 + c_0 a +
+    (c_2 s - c_4) ... written out below; both roots are returned (complex128
+    points satisfying cyclic-4 and the slice to working precision before the
+    tracker's t = 0 Newton polish).  Raises ValueError on a degenerate quadratic."""
+    c0, c1, c2, c3, c4 = [complex(v) for v in slice_row]
+    s = 1.0 if family == 1 else -1.0
+    # x = (a, s/a, -a, -s/a):  c0 + c1 a + c2 s/a - c3 a - c4 s/a = 0
+    #   -> (c1 - c3) a^2 + c0 a + s (c2 - c4) = 0
+    qa, qb, qc = c1 - c3, c0, s * (c2 - c4)
+    if abs(qa) < 1e-14 and abs(qc) < 1e-14:
+        raise ValueError("degenerate slice for the cyclic-4 witness: resample L")
+    roots = np.roots([qa, qb, qc]) if abs(qa) >= 1e-14 else np.array([-qc / qb])
+    # a = 0 is not a point of the family (x_1 = s/a): it appears only when the slice has c2 = c4
+    return [np.array([a, s / a, -a, -s / a], dtype=np.complex128) for a in roots if abs(a) > 1e-14]
+
+
+def slice_rows(aug: PolynomialSystem, dim: int) -> np.ndarray:
+    """The last `dim` affine equations of `aug` as rows (c_0, c_1, ..., c_n)."""
+    n, N = aug.n_vars, aug.n_eqs
+    out = np.zeros((dim, n + 1), dtype=np.complex128)
+    for r in range(dim):
+        for sup, coef in aug.terms(N - dim + r):
+            out[r, 0 if not sup else sup[0][0] + 1] += coef
+    return out
+
+
 def cyclic_leg(m: int, prec: PrecisionMode, seed_l: int = 1, seed_k: int = 2, seed_gamma: int = 3) -> Workload:
     """Monodromy leg h = alpha (1-t) (f, L) + t (f, K), k = 1."""
     n = m * m

@@ -36,3 +36,38 @@ def random_operands(prec: int, count: int, seed: int, positive=False, small_int=
             r = oracle.arith(prec, OPS["renorm"], flat, flat)
             out[:, c] = r[:, 0]
     return out
+
+
+def edge_operands(prec: int, count: int, seed: int, positive=False, oracle=None):
+    """Operands across the whole binary64 range (SURVEY / VERDICT r1): leading
+    limbs with exponents in [-1074, 1023] (huge, tiny and subnormal values),
+    plus +-0, +-inf, NaN, the largest finite value and values just inside the
+    glibc hypot scaling thresholds (2^511, 2^-459); lower limbs scaled below
+    ulp/2 (so they underflow near the bottom of the range) and the DD / QD
+    values renormalised through `oracle` when given."""
+    L = (1, 2, 4)[prec]
+    rng = np.random.default_rng(seed)
+    out = np.zeros((count, 2, L))
+    specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 2.2250738585072014e-308, 1.7976931348623157e308,
+                         2.0 ** 511, 2.0 ** 512, 2.0 ** -459, 2.0 ** -460, 3.0e300, 1.0e-300, 1.0])
+    for c in range(2):
+        hi = rng.uniform(0.5, 1.0, count) * np.exp2(rng.integers(-1074, 1024, count).astype(float))
+        hi *= np.where(rng.uniform(size=count) < 0.5, -1.0, 1.0)
+        pick = rng.uniform(size=count) < 0.2
+        hi[pick] = rng.choice(specials, size=int(pick.sum()))
+        if positive:
+            hi = np.abs(hi)
+            hi[np.isnan(hi)] = 1.0
+        out[:, c, 0] = hi
+        scale = np.abs(hi)
+        with np.errstate(invalid="ignore", over="ignore"):
+            for l in range(1, L):
+                scale = scale * 2.0 ** -53
+                out[:, c, l] = np.where(np.isfinite(scale), rng.uniform(-1, 1, count) * scale, 0.0)
+    if oracle is not None and L > 1:
+        for c in range(2):
+            flat = np.zeros((count, 2, L))
+            flat[:, 0] = out[:, c]
+            r = oracle.arith(prec, OPS["renorm"], flat, flat)
+            out[:, c] = r[:, 0]
+    return out

@@ -29,6 +29,14 @@ def ref_oracle():
 
 
 @pytest.fixture(scope="session")
+def ref_oracle_or_restated():
+    """The reference-header oracle where it was built (oracle/_ref travels
+    with gpurun), else the restatement (pinned to it by the CPU suite)."""
+    from oracle.orc import REFERENCE, Oracle
+    return Oracle("reference" if os.path.exists(REFERENCE) else "restatement")
+
+
+@pytest.fixture(scope="session")
 def gpu():
     from paper_1501_06625_b200 import device_count
     if device_count() == 0:
@@ -45,3 +53,15 @@ def assert_bits_equal(a, b, what=""):
     assert a.shape == b.shape, (what, a.shape, b.shape)
     bad = np.flatnonzero(a.reshape(-1) != b.reshape(-1))
     assert bad.size == 0, f"{what}: {bad.size} of {a.size} limbs differ (first at {bad[:5]})"
+
+
+def assert_bits_equal_nan(a, b, what=""):
+    """Bitwise equality where any two NaNs count as equal: the GPU's FP64
+    units return the canonical NaN, x86 propagates the operand's payload
+    (DESIGN.md section 3); every non-NaN limb must match bit for bit."""
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    both_nan = np.isnan(a) & np.isnan(b)
+    bad = np.flatnonzero((a.view(np.uint64) != b.view(np.uint64)) & ~both_nan)
+    assert bad.size == 0, f"{what}: {bad.size} of {a.size} limbs differ (first at {bad[:5]}: {a[bad[:3]]} vs {b[bad[:3]]})"

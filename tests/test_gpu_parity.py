@@ -7,8 +7,8 @@ summation trees, so any difference is a bug.
 import numpy as np
 import pytest
 
-from conftest import assert_bits_equal
-from arith_inputs import OPS, random_operands
+from conftest import assert_bits_equal, assert_bits_equal_nan
+from arith_inputs import OPS, edge_operands, random_operands
 
 import paper_1501_06625_b200 as pt
 from paper_1501_06625_b200 import PrecisionMode as PM
@@ -33,6 +33,23 @@ def test_arith_device_bitwise(gpu, oracle, prec, op):
     elif op in ("add", "sub", "mul", "mul_d", "div", "sqrt", "renorm", "norm_sqr", "powi"):
         want, got = want[:, 0], got[:, 0]
     assert_bits_equal(got, want, f"{prec.name} {op}")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=lambda p: p.name)
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "mul_d", "div", "sqrt", "renorm", "cmul", "cadd",
+                                "conj_mul", "norm_sqr", "modulus_double", "cscale"])
+def test_arith_device_edge_operands(gpu, ref_oracle_or_restated, prec, op):
+    """The whole binary64 range: exponents -1074..1023, subnormals, +-0,
+    +-inf, NaN, the glibc hypot scaling thresholds.  Bitwise against the
+    reference-header oracle (NaN payloads aside), non-finite DD values
+    included (dd_norm's {h, 0} rule, multiprec.hpp:102-107)."""
+    orc = ref_oracle_or_restated
+    count = 4096 if prec == PM.QD else 20000
+    a = edge_operands(int(prec), count, 11, positive=(op == "sqrt"), oracle=orc)
+    b = edge_operands(int(prec), count, 12, oracle=orc)
+    want = orc.arith(int(prec), OPS[op], a, b)
+    got = pt.arith(prec, OPS[op], a, b, device=gpu)
+    assert_bits_equal_nan(got, want, f"{prec.name} {op} (edge operands)")
 
 
 def _perturbed(w, scale=1e-3, seed=0):

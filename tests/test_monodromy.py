@@ -27,6 +27,14 @@ def oracle_tracker(orc):
     return run
 
 
+def oracle_evaluator(orc):
+    def run(sysm, points):
+        one = np.zeros(2 * sysm.prec.limbs)
+        one[0] = 1.0
+        return np.array([orc.eval_homotopy(int(sysm.prec), sysm, sysm, one, 1, p, 1.0)[2] for p in points])
+    return run
+
+
 def witness(m, prec):
     n, dim = m * m, m - 1
     fL = augment_with_linear(n, dim, 1, prec)
@@ -47,19 +55,38 @@ def residual(sys_, x):
     return worst
 
 
-def test_cyclic4_family1_has_degree_2(oracle):
-    fL, w0 = witness(2, PM.DD)
-    ws = MD.monodromy_degree(4, 1, [w0], seed=11, stabilization_loops=3, prec=PM.DD,
-                             tracker=oracle_tracker(oracle))
+@pytest.mark.parametrize("prec", [PM.D, PM.DD], ids=lambda p: p.name)
+def test_cyclic4_family1_has_degree_2(oracle, prec):
+    """Acceptance criterion 2: one internally constructed family-1 witness
+    point (cyclic4_witness) stabilises at exactly 2 points,
+    every stored point's (f, L) residual below the corrector tolerance."""
+    fL = augment_with_linear(4, 1, 1, prec)
+    pts = W.cyclic4_witness(W.slice_rows(fL, 1)[0], family=1)
+    assert all(residual(fL, limbs_from_complex(p, prec)) < 1e-12 for p in pts)
+    w0 = limbs_from_complex(pts[0], prec)
+    # polish to working precision with the tracker's t = 0 Newton pass
+    ends, ok = oracle_tracker(oracle)(fL, fL, np.r_[1.0, np.zeros(2 * prec.limbs - 1)], w0[None],
+                                      MD.StepControlParams.defaults(prec))
+    ws = MD.monodromy_degree(4, 1, [ends[0]], seed=11, stabilization_loops=3, prec=prec,
+                             tracker=oracle_tracker(oracle), evaluator=oracle_evaluator(oracle))
     assert ws.degree == 2
-    for p in ws.points:
-        assert residual(fL, p) < 1e-10
+    tol = MD.StepControlParams.defaults(prec).newton_tol
+    assert all(r < tol for r in ws.residuals[1:]) and len(ws.residuals) == 2
+
+
+def test_cyclic4_witness_spec_examples():
+    # family 1 at a = i is (i, -i, -i, i), a cyclic-4 root (SPEC.md:560)
+    row = np.array([-1j, 1, 0, 0, 0], dtype=complex)  # the slice x_0 - i = 0
+    pts = W.cyclic4_witness(row, 1)
+    assert any(np.allclose(p, [1j, -1j, -1j, 1j]) for p in pts)
+    with pytest.raises(ValueError):  # c1 = c3, c2 = c4 in our indexing (constant first): vanishing quadratic
+        W.cyclic4_witness(np.array([1, 0.5, 0.25, 0.5, 0.25], dtype=complex), 1)
 
 
 def test_zero_stabilization_loops_returns_start(oracle):
     _, w0 = witness(2, PM.DD)
     ws = MD.monodromy_degree(4, 1, [w0], seed=11, stabilization_loops=0, prec=PM.DD,
-                             tracker=oracle_tracker(oracle))
+                             tracker=oracle_tracker(oracle), evaluator=oracle_evaluator(oracle))
     assert ws.degree == 1 and ws.loops == 0
     assert np.array_equal(ws.points[0].view(np.uint64), w0.view(np.uint64))
 
@@ -84,17 +111,23 @@ def test_gpu_loop_bitwise_equals_oracle(gpu, oracle):
 
 
 @pytest.mark.gpu
-def test_gpu_cyclic16_monodromy_stays_on_the_backelin_family(gpu):
-    """SPEC.md:581 expects degree 4 (Table 5).  Our loops (bit-equal to
-    the oracle's, test above) stabilise at 8 points, all on the witness's
-    Backelin family x_{4a+b} = i^a r_b (prod x = 1) and on (f, L): recorded in
-    DESIGN.md section 8 as an open question on the component structure."""
+def test_gpu_cyclic16_monodromy_degree_is_4(gpu):
+    """SPEC.md:581 / PAPER.md Table 5: the cyclic-16 Backelin component has
+    degree 4.  The family x_{4a+b} = i^a r_b with prod x = 1 is the union of 4
+    components {prod r = zeta, zeta^4 = 1}; the loops' endpoints that jump to a
+    sibling component (prod r changes) are path-crossing failures and are
+    rejected by the component key, so the witness set stabilises at the
+    start component's 4 points, all on (f, L) below the corrector tolerance."""
     fL, w0 = witness(4, PM.DD)
+    key = W.backelin_component_key(4)
     ws = MD.monodromy_degree(16, 3, [w0], seed=3, stabilization_loops=4, prec=PM.DD,
-                             tracker=MD.gpu_batch_tracker(gpu))
-    assert ws.degree >= 4 and ws.degree % 4 == 0 and ws.failed_paths == 0
+                             tracker=MD.gpu_batch_tracker(gpu), evaluator=MD.gpu_evaluator(gpu),
+                             component_key=key, residual_tol=1e-12)
+    assert ws.degree == 4, ws.log
+    k0 = key(ws.points[0])
     for p in ws.points:
         assert residual(fL, p) < 1e-10
+        assert abs(key(p) - k0) < 1e-9
         z = complex_from_limbs(p)
         for b in range(4):
             for a in range(4):
