@@ -1,23 +1,34 @@
 #!/usr/bin/env python
-"""bench.py -- BASELINE.json metric on B200: tracked paths per second
-(= 1 / seconds per tracked path) for the Chandrasekhar H dim-64 single path
-in double-double (configs[1]); other configs via --workload / --prec.
+"""bench.py -- BASELINE.json metric on B200.
+
+Default line (no flags): "paths/sec/box" on configs[4], the batch of 8192
+independent paths of the dim-32 random degree-4 system (M = 512) in
+double-double -- the workload that shards across GPUs.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload chandra64|cyclic16|rand96|cyclic256|batch32] [--prec d|dd|qd]
+                  [--workload batch32|chandra64|cyclic16|rand96|cyclic256] [--prec d|dd|qd]
 
-A step is one tracked path (single-path workloads) or one pass over the whole
-batch (batch32).  Single paths do not shard: at N > 1 every rank tracks its
-own replica ("replicas only") and value counts all ranks'
-paths; batch32 shards the 8192 paths contiguously over the ranks.
-value:  device time (CUDA events on the launching stream, inputs resident,
-        L2 flushed between steps, max over ranks).
-e2e:    the same metric through the C-ABI pt_track_path / pt_track_batch with
-        pinned host buffers (H2D of the start, D2H of end point and stats
-        inside the timed region), wall clock, max over ranks.
-roofline: algorithmic FP64 instructions of the reference DD/QD algorithms per
-        launch (pt_plan_work x the path's evaluation / solve / step counts)
-        over the measured FP64 DFMA peak (profiles/fp64_peak.json).
+A step (batch) is one k_track_batch launch over a fixed slice of
+--paths-per-step (2048) paths per rank: at step s rank r tracks paths
+[((s N + r) P) mod 8192, +P) (multi.step_slice) -- weak scaling, N ranks
+cover N slices per step, no collective on the data path.  A step
+(single-path workloads) is one tracked path; at N > 1 each rank tracks a
+replica ("replicas only").
+
+value:  paths per second over all ranks, device time (CUDA events on the
+        launching stream, inputs resident in HBM, L2 flushed between steps
+        by a 256 MiB write, max over ranks).
+e2e:    the same metric through the public C-ABI pt_track_batch /
+        pt_track_path with pinned host buffers: H2D of the starts and D2H of
+        the end points and stats inside the timed region (wall clock, max
+        over ranks).
+roofline: FP64-pipe bound -- algorithmic FP64 instructions of the reference
+        DD/QD algorithms per launch (pt_plan_work x each path's evaluation /
+        solve / step counts) over the launch time, against the measured DFMA
+        peak (profiles/fp64_peak.json).
+cpu_baseline: the SPEC tracker on the unmodified reference headers
+        (oracle/_ref) on this host's cores -- a thread pool over paths for the
+        batch, plus the 1-thread single-path figure (i).
 """
 import argparse
 import ctypes as C
@@ -34,7 +45,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-METRIC = "tracked paths/s (1 / sec per tracked path); chandra64 dd single path"
+BATCH_METRIC = "paths/sec/box; batch of 8192 dim-32 random degree-4 paths (M=512), dd"
 
 
 def parse():
@@ -43,10 +54,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="chandra64")
+    ap.add_argument("--workload", default="batch32")
     ap.add_argument("--prec", default=None)
+    ap.add_argument("--paths-per-step", type=int, default=2048, help="batch: paths per rank per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-paths", type=int, default=96, help="batch: CPU sample paths per reference step")
     ap.add_argument("--no-cpu-reference", action="store_true",
                     help="skip the precision-matched CPU tracker timing (keep the CPU-D comparison)")
     ap.add_argument("--max-steps", type=int, default=None,
@@ -58,7 +71,12 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def is_batch(args):
+    return args.workload == "batch32"
+
+
 def workload(args):
+    """Inputs only (libpt_inputs.so): never loads the tracker library."""
     from paper_1501_06625_b200 import PrecisionMode, workloads as W
     prec = PrecisionMode.parse(args.prec) if args.prec else None
     if args.workload == "cyclic16":
@@ -81,12 +99,26 @@ def apply_overrides(args, w):
     return w
 
 
+def metric_of(args, w):
+    if is_batch(args) and w.prec.name == "DD":
+        return BATCH_METRIC
+    return f"tracked paths/s (1 / sec per tracked path); {w.name}"
+
+
 def config(args, w, world):
     cfg = {"workload": w.name, "n_vars": w.n, "n_eqs": w.N, "precision": w.prec.name.lower(),
-           "paths_per_step": int(w.starts.shape[0]) if args.workload == "batch32" else world,
-           "parallelism": ("shard" if args.workload == "batch32" else "replicas") + f"x{world}",
            "l2": "flushed between steps (256 MiB write)"}
+    if is_batch(args):
+        cfg.update({"batch_paths": int(w.starts.shape[0]), "paths_per_step_per_gpu": args.paths_per_step,
+                    "paths_per_step": args.paths_per_step * world,
+                    "parallelism": f"batch shards x{world} (multi.step_slice, no collective)"})
+    else:
+        cfg.update({"paths_per_step": world, "parallelism": f"replicas x{world}"})
     return cfg
+
+
+def dtype_of(w):
+    return {"D": "f64", "DD": "dd (2xf64)", "QD": "qd (4xf64)"}[w.prec.name]
 
 
 class Clocks:
@@ -164,11 +196,9 @@ def path_work(hom, stats_list, degree):
 
 
 def critical_path(hom, st, prof, steps):
-    """Latency view of a single path (the FP64-pipe fraction is tiny by
-    construction): the MGS sweep is a chain of n dependent column steps
-    (project column k+1 with q_k, normalise it, hand q_{k+1} on).  From the
-    device timeline of the last sweep: median ns per column step, and the
-    share of the measured MGS time that n x solves x that step explains."""
+    """Latency view of a single path: the MGS sweep is a chain of n dependent
+    column steps; from the device timeline of the last sweep: median ns per
+    column step and the share of the measured MGS time it explains."""
     from paper_1501_06625_b200 import _native as nat
     n = hom.n
     buf = np.zeros(6 * (n + 1))
@@ -186,45 +216,59 @@ def critical_path(hom, st, prof, steps):
             "mgs_share_of_phases": float(prof[2] / sum(prof[:5])) if sum(prof[:5]) > 0 else None}
 
 
-def cpu_reference(args, w, seconds):
-    """The reference CPU tracker on this host's cores: oracle/_ref (SPEC
-    tracker on the unmodified reference headers), else the oracle port."""
+# ---------------------------------------------------------------------------
+# CPU baselines (oracle/_ref: the SPEC tracker on the unmodified reference
+# arithmetic headers; the oracle restatement where _ref was not built)
+# ---------------------------------------------------------------------------
+def _oracle():
     from oracle.orc import Oracle
-    orc = Oracle("auto")
+    return Oracle("auto")
+
+
+def cpu_batch_pool(w, n_paths, offset=0):
+    """(iii): a thread pool over paths on all host cores, one single-threaded
+    tracker per path."""
+    orc = _oracle()
     threads = os.cpu_count() or 1
+    idx = (offset + np.arange(n_paths)) % w.starts.shape[0]
+    starts = np.ascontiguousarray(w.starts[idx])
+    t0 = time.perf_counter()
+    _, stats = orc.track_batch(int(w.prec), w.g, w.f, w.gamma, w.k, starts, w.params, threads)
+    dt = time.perf_counter() - t0
+    kind = "reference" if orc.variant == "reference" else "port"
+    return {"value": n_paths / dt, "unit": "paths/s", "cores": threads, "kind": kind,
+            "sample": f"{n_paths} paths [{int(idx[0])}..) of {w.name} in {dt:.2f}s on a pool of {threads} host "
+                      f"threads, one single-threaded tracker per path "
+                      f"({'oracle/_ref: SPEC tracker on the unmodified reference headers' if kind == 'reference' else 'oracle restatement'})",
+            "paths_ok": int(sum(s.status == 0 for s in stats))}
+
+
+def cpu_single(w, seconds, threads):
+    """(i) one path on 1 thread, or (ii) one path with OpenMP inside it."""
+    orc = _oracle()
     orc.set_threads(threads)
-    starts = w.starts if args.workload == "batch32" else w.starts[:1]
     done, t0 = 0, time.perf_counter()
-    stats = None
+    p = 0
     while True:
-        for p in range(starts.shape[0]):
-            _, stats, _ = orc.track_path(int(w.prec), w.g, w.f, w.gamma, w.k, starts[p], w.params)
-            done += 1
-            if time.perf_counter() - t0 > seconds:
-                break
+        orc.track_path(int(w.prec), w.g, w.f, w.gamma, w.k, w.starts[p % w.starts.shape[0]], w.params)
+        done += 1
+        p += 1
         if time.perf_counter() - t0 > seconds:
             break
     dt = time.perf_counter() - t0
     kind = "reference" if orc.variant == "reference" else "port"
-    sample = (f"{done} tracked path(s) of {w.name} in {dt:.2f}s with {threads} OpenMP threads "
-              f"({'SPEC tracker on the unmodified reference arithmetic headers, oracle/_ref' if kind == 'reference' else 'oracle restatement'})")
-    return {"value": done / dt, "unit": "paths/s", "cores": threads, "kind": kind, "sample": sample,
-            "last_steps": stats.steps if stats else None}
+    return {"value": done / dt, "unit": "paths/s", "cores": threads, "kind": kind,
+            "sample": f"{done} tracked path(s) of {w.name} in {dt:.2f}s, {threads} OpenMP thread(s) inside the path"}
 
 
 def cpu_d_all_cores(args, seconds=2.0):
-    """North-star comparison: the reference CPU tracker in complex DOUBLE on
-    all host cores, same system and prefix (--max-steps): seconds per tracked
-    path and per Newton iteration (the per-iteration figure is the fair one
-    for prefixes, whose step counts differ between precisions)."""
+    """North-star comparison for single paths: the reference CPU tracker in
+    complex DOUBLE on all host cores, same system and prefix (--max-steps)."""
     from paper_1501_06625_b200 import PrecisionMode
-    from oracle.orc import Oracle
     a = argparse.Namespace(**vars(args))
     a.prec = "d"
     wd = apply_overrides(a, workload(a))
-    if args.workload == "batch32":
-        return None
-    orc = Oracle("auto")
+    orc = _oracle()
     orc.set_threads(os.cpu_count() or 1)
     n, iters, t0 = 0, 0, time.perf_counter()
     while True:
@@ -239,24 +283,34 @@ def cpu_d_all_cores(args, seconds=2.0):
 
 
 def run_reference(args):
+    """--impl reference: the reference CPU tracker (oracle/_ref) on the box's
+    host cores, same metric/config/unit; rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     w = apply_overrides(args, workload(args))
-    per_step = max(args.cpu_seconds / max(args.steps, 1), 0.5)
     vals = []
-    for _ in range(args.warmup):
-        cpu_reference(args, w, 0.1)
-    for _ in range(args.steps):
-        vals.append(cpu_reference(args, w, per_step))
+    if is_batch(args):
+        for s in range(args.warmup):
+            cpu_batch_pool(w, min(16, args.cpu_paths), offset=s * 16)
+        for s in range(args.steps):
+            vals.append(cpu_batch_pool(w, args.cpu_paths, offset=s * args.cpu_paths))
+    else:
+        per_step = max(args.cpu_seconds / max(args.steps, 1), 0.5)
+        threads = os.cpu_count() or 1
+        for _ in range(args.warmup):
+            cpu_single(w, 0.1, threads)
+        for _ in range(args.steps):
+            vals.append(cpu_single(w, per_step, threads))
     value = sum(v["value"] for v in vals) / len(vals)
     base = vals[-1]
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": {"D": "f64", "DD": "dd (2xf64)", "QD": "qd (4xf64)"}[w.prec.name],
+    line = {"impl": "reference", "metric": metric_of(args, w), "value": value, "unit": "paths/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(w),
             "data": "synthetic (pinned generators, SURVEY.md 8(d))", "config": config(args, w, 1),
             "cpu_baseline": {**{k: base[k] for k in ("unit", "cores", "kind", "sample")}, "value": value},
             "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line["ms_per_step"] = 1e3 * (args.cpu_paths if is_batch(args) else 1) / value
     print(json.dumps(line))
 
 
@@ -271,33 +325,35 @@ def run_ours(args):
     torch.cuda.set_device(device)
     import paper_1501_06625_b200 as pt
     from paper_1501_06625_b200 import _native as nat
+    from paper_1501_06625_b200.multi import step_slice
 
     w = apply_overrides(args, workload(args))
-    L, n = w.prec.limbs, w.n
-    batch = args.workload == "batch32"
+    batch = is_batch(args)
     hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=device)
     sp = w.params.native()
     stream = torch.cuda.Stream(device)  # kernel and its CUDA events on the same stream
     sh = C.c_void_p(stream.cuda_stream)
-    if batch:
-        P = w.starts.shape[0]
-        lo, hi = rank * P // world, (rank + 1) * P // world
-        starts_h = w.starts[lo:hi]
-    else:
-        starts_h = w.starts[:1]
-    npaths = starts_h.shape[0]
-    d_start = torch.from_numpy(np.ascontiguousarray(starts_h)).to(f"cuda:{device}")
-    d_end = torch.zeros_like(d_start)
-    d_stats = torch.zeros((npaths, C.sizeof(nat.PathStats)), dtype=torch.uint8, device=f"cuda:{device}")
+    PS = 2 * w.prec.limbs * w.n  # doubles per start point
+    total_batch = w.starts.shape[0]
+    P = args.paths_per_step if batch else 1
+    # every start resident in HBM; each step points into its slice
+    d_all = torch.from_numpy(np.ascontiguousarray(w.starts if batch else w.starts[:1])).to(f"cuda:{device}")
+    d_end = torch.zeros((P,) + tuple(w.starts.shape[1:]), dtype=torch.float64, device=f"cuda:{device}")
+    d_stats = torch.zeros((P, C.sizeof(nat.PathStats)), dtype=torch.uint8, device=f"cuda:{device}")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
 
-    def launch():
+    def slice_of(step):
+        return step_slice(total_batch, P, step, rank, world) if batch else (0, 1)
+
+    def launch(step):
+        lo, _ = slice_of(step)
+        src = C.c_void_p(d_all.data_ptr() + lo * PS * 8)
         if batch:
-            nat.check(nat.lib.pt_track_batch_device(hom.plan, npaths, C.c_void_p(d_start.data_ptr()), C.byref(sp),
-                                                    C.c_void_p(d_end.data_ptr()), C.c_void_p(d_stats.data_ptr()), sh))
+            nat.check(nat.lib.pt_track_batch_device(hom.plan, P, src, C.byref(sp), C.c_void_p(d_end.data_ptr()),
+                                                    C.c_void_p(d_stats.data_ptr()), sh))
         else:
-            nat.check(nat.lib.pt_track_path_device(hom.plan, C.c_void_p(d_start.data_ptr()), C.byref(sp),
-                                                   C.c_void_p(d_end.data_ptr()), C.c_void_p(d_stats.data_ptr()), sh))
+            nat.check(nat.lib.pt_track_path_device(hom.plan, src, C.byref(sp), C.c_void_p(d_end.data_ptr()),
+                                                   C.c_void_p(d_stats.data_ptr()), sh))
 
     def barrier():
         torch.cuda.synchronize(device)
@@ -306,45 +362,56 @@ def run_ours(args):
         torch.cuda.synchronize(device)
 
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            launch()
+        for s in range(args.warmup):
+            launch(s)
     barrier()
     clocks = Clocks(device)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     prof = np.zeros(8)
     nat.check(nat.lib.pt_plan_profile(hom.plan, nat.dptr(prof), 1))
-    for e0, e1 in ev:
+    stats_all = []
+    for s, (e0, e1) in enumerate(ev):
         with torch.cuda.stream(stream):
             flush.zero_()
             e0.record(stream)
-            launch()
+            launch(s)
             e1.record(stream)
+            if batch:  # per-step statistics feed the work count (stream-ordered copy, outside the events)
+                stats_all.append((s, d_stats.clone()))
     barrier()
     nat.check(nat.lib.pt_plan_profile(hom.plan, nat.dptr(prof), 1))
     clk = clocks.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     t_dev = sum(step_ms) / 1e3
-    stats_raw = d_stats.cpu().numpy()
-    stats_list = [nat.PathStats.from_buffer_copy(stats_raw[p].tobytes()) for p in range(npaths)]
+    if batch:
+        stats_list = []
+        for _, t in stats_all:
+            raw = t.cpu().numpy()
+            stats_list.extend(nat.PathStats.from_buffer_copy(raw[p].tobytes()) for p in range(P))
+    else:
+        raw = d_stats.cpu().numpy()
+        stats_list = [nat.PathStats.from_buffer_copy(raw[0].tobytes())]
 
-    # e2e through the public C-ABI with pinned host buffers
-    h_start = torch.from_numpy(np.ascontiguousarray(starts_h)).pin_memory()
-    h_end = torch.zeros_like(h_start).pin_memory()
-    h_stats = (nat.PathStats * npaths)()
-    dp = lambda t: C.cast(C.c_void_p(t.data_ptr()), nat._dp)
+    # e2e through the public C-ABI with pinned host buffers (H2D starts, D2H ends + stats per step)
+    h_starts = torch.from_numpy(np.ascontiguousarray(w.starts if batch else w.starts[:1])).pin_memory()
+    h_end = torch.zeros((P,) + tuple(w.starts.shape[1:]), dtype=torch.float64).pin_memory()
+    h_stats = (nat.PathStats * P)()
+    dp = lambda t, off=0: C.cast(C.c_void_p(t.data_ptr() + off), nat._dp)
+    e2e_steps = max(2, args.steps // 5) if batch else args.steps
 
-    def e2e_call():
+    def e2e_call(step):
+        lo, _ = slice_of(step)
         if batch:
-            nat.check(nat.lib.pt_track_batch(hom.plan, npaths, dp(h_start), C.byref(sp), dp(h_end), h_stats))
+            nat.check(nat.lib.pt_track_batch(hom.plan, P, dp(h_starts, lo * PS * 8), C.byref(sp), dp(h_end), h_stats))
         else:
-            nat.check(nat.lib.pt_track_path(hom.plan, dp(h_start), C.byref(sp), dp(h_end), h_stats))
+            nat.check(nat.lib.pt_track_path(hom.plan, dp(h_starts), C.byref(sp), dp(h_end), h_stats))
 
-    e2e_call()
+    e2e_call(0)
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_call()
+    for s in range(e2e_steps):
+        e2e_call(s)
     t_e2e = time.perf_counter() - t0
     barrier()
 
@@ -352,58 +419,63 @@ def run_ours(args):
     if world > 1:
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
     t_dev_max, t_e2e_max = float(tt[0]), float(tt[1])
-    total_paths = (w.starts.shape[0] if batch else world) * args.steps
-    value = total_paths / t_dev_max
-    e2e_value = total_paths / t_e2e_max
+    paths_per_step = P * world
+    value = paths_per_step * args.steps / t_dev_max
+    e2e_value = paths_per_step * e2e_steps / t_e2e_max
 
     if rank == 0:
         work, we, ws = path_work(hom, stats_list, w.params.pred_degree)
         t_launch = t_dev / args.steps
         peak, peak_src = fp64_peak()
-        achieved = work / t_launch
+        achieved = work / args.steps / t_launch
         traffic = None
         tr_path = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr_path):
             with open(tr_path) as fh:
                 traffic = json.load(fh).get(w.name)
-        ok = all(s.status == 0 for s in stats_list)
+        ok = [s.status == 0 for s in stats_list]
         line = {
-            "metric": METRIC if args.workload == "chandra64" and w.prec.name == "DD" else
-            f"tracked paths/s; {w.name}",
+            "metric": metric_of(args, w),
             "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_dev_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if batch else "weak", "vs_baseline": None,
-            "dtype": {"D": "f64", "DD": "dd (2xf64)", "QD": "qd (4xf64)"}[w.prec.name],
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(w),
             "data": "synthetic (pinned generators, SURVEY.md 8(d)); no checkpoints",
             "config": config(args, w, world),
-            "sec_per_path": t_dev_max / args.steps / (npaths if batch else 1),
-            "path": {"success": ok, "steps": stats_list[0].steps, "newton_iters": stats_list[0].newton_iters,
-                     "solves": stats_list[0].solves, "grid_ctas": hom.info(4), "engine": hom.engine,
-                     "cluster_ctas": hom.info(9), "paths_ok": int(sum(s.status == 0 for s in stats_list)),
-                     "paths": len(stats_list)},
+            "sec_per_path": t_dev_max / args.steps / P,
+            "paths": {"tracked": len(stats_list), "ok": int(sum(ok)),
+                      "mean_steps": float(np.mean([s.steps for s in stats_list])),
+                      "mean_newton_iters": float(np.mean([s.newton_iters for s in stats_list])),
+                      "engine": "batch" if batch else hom.engine, "ctas": hom.info(6 if batch else 4)},
             "e2e": {"value": e2e_value, "unit": "paths/s",
-                    "h2d_bytes_per_step": int(h_start.numel() * 8),
-                    "d2h_bytes_per_step": int(h_end.numel() * 8 + C.sizeof(nat.PathStats) * npaths),
-                    "timing": "wall clock around the C-ABI call, max over ranks"},
+                    "h2d_bytes_per_step": int(P * PS * 8),
+                    "d2h_bytes_per_step": int(P * PS * 8 + C.sizeof(nat.PathStats) * P),
+                    "steps": e2e_steps, "timing": "wall clock around the C-ABI call, max over ranks"},
             "roofline": {"bound": "fp64-pipe",
-                         "kernel": "k_track_batch" if batch else ("k_track_cluster" if hom.engine == "cluster" else "k_track_grid"),
+                         "kernel": "k_track_batch" if batch else ("k_track_cluster" if hom.engine == "cluster"
+                                                                  else "k_track_grid"),
                          "achieved": achieved * 1e-12, "peak": peak * 1e-12,
                          "unit": "T FP64-instr/s (DADD/DMUL/DFMA of the reference DD/QD algorithms; FMA = 1)",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "work_per_launch_fp64_instr": work, "work_per_eval": we, "work_per_solve": ws},
+                         "work_per_launch_fp64_instr": work / args.steps, "work_per_eval": we, "work_per_solve": ws},
             "gpu_launches": args.steps,
-            "phase_ms_per_path": None if batch else {
-                k: prof[i] * 1e-6 / args.steps for i, k in enumerate(
-                    ["monomials", "slot_sums", "mgs", "backsub_update", "predict"])},
-            "newton_iters_timed": None if batch else prof[5] / args.steps,
-            "critical_path": None if batch else critical_path(hom, stats_list[0], prof, args.steps),
             "clocks": clk,
         }
+        if not batch:
+            line["path"] = {"success": bool(ok[0]), "steps": stats_list[0].steps,
+                            "newton_iters": stats_list[0].newton_iters, "solves": stats_list[0].solves}
+            line["phase_ms_per_path"] = {k: prof[i] * 1e-6 / args.steps for i, k in enumerate(
+                ["monomials", "slot_sums", "mgs", "backsub_update", "predict"])}
+            line["critical_path"] = critical_path(hom, stats_list[0], prof, args.steps)
         if world == 1 and not args.no_cpu_baseline:
-            if not args.no_cpu_reference:
-                line["cpu_baseline"] = cpu_reference(args, w, args.cpu_seconds)
-            dall = cpu_d_all_cores(args)
-            if dall is not None:
+            if batch:
+                line["cpu_baseline"] = cpu_batch_pool(w, args.cpu_paths)
+                one = cpu_single(w, min(args.cpu_seconds, 5.0), 1)
+                line["cpu_single_thread"] = one
+            else:
+                if not args.no_cpu_reference:
+                    line["cpu_baseline"] = cpu_single(w, args.cpu_seconds, os.cpu_count() or 1)
+                    line["cpu_single_thread"] = cpu_single(w, min(args.cpu_seconds, 5.0), 1)
+                dall = cpu_d_all_cores(args)
                 line["cpu_d_all_cores"] = dall
                 line["sec_per_newton_iter"] = t_dev_max / args.steps / max(1, stats_list[0].newton_iters)
         print(json.dumps(line))

@@ -76,7 +76,7 @@ Point<Real> from_limbs(const std::vector<double>& v, size_t n) {
 template <class Real>
 struct System {
   int n_vars = 0;
-  std::vector<int32_t> eq_ptr{0}, term_ptr{0}, var, exp;
+  std::vector<int32_t> eq_ptr{0, 0}, term_ptr{0}, var, exp;  // one open equation: [start, running end]
   std::vector<Complex<Real>> coef;
 
   // add one term (support: (var, exp) with var ascending) to the last equation

@@ -21,6 +21,20 @@ def shard_range(n_paths: int, rank: int, world: int) -> Tuple[int, int]:
     return rank * n_paths // world, (rank + 1) * n_paths // world
 
 
+def step_slice(n_paths: int, per_rank: int, step: int, rank: int, world: int) -> Tuple[int, int]:
+    """Weak-scaling bench slices (bench.py): at step s rank r tracks the
+    contiguous paths [lo, lo + per_rank) of the batch with
+    lo = ((s * world + r) * per_rank) mod n_paths, so every rank owns a fixed
+    amount of work per step and N ranks together cover N slices; per_rank
+    must divide n_paths (slices never wrap)."""
+    if per_rank < 1 or n_paths % per_rank:
+        raise ValueError("per_rank must divide n_paths")
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    lo = ((step * world + rank) * per_rank) % n_paths
+    return lo, lo + per_rank
+
+
 def track_batch_sharded(track: Callable[[np.ndarray], Tuple[np.ndarray, List]], starts: np.ndarray,
                         rank: int, world: int, group=None) -> Optional[Tuple[np.ndarray, np.ndarray]]:
     """Track this rank's shard with `track(starts_shard) -> (ends, stats)` and

@@ -21,6 +21,11 @@ int main() {
   g.term({{0, 1}}, Complex<R>(R(1.0)));
   f.term({}, Complex<R>(R(-2.0)));
   f.term({{0, 1}}, Complex<R>(R(1.0)));
+  {  // the canonical-form view the C-ABI receives (one equation, two terms)
+    std::vector<double> limbs;
+    const pt_system_desc d = g.desc(limbs);
+    if (d.n_eqs != 1 || d.n_terms != 2 || d.eq_ptr[0] != 0 || d.eq_ptr[1] != 2 || d.term_ptr[2] != 1) return 4;
+  }
   Point<R> x0{Complex<R>(R(1.0))};
   auto rt = b200::from_limbs<R>(b200::to_limbs<R>(x0), 1);
   if (!(rt[0].re.hi == 1.0 && rt[0].re.lo == 0.0)) return 3;

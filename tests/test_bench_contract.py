@@ -37,9 +37,26 @@ def test_reference_arm_contract():
     assert "workload" in d["config"]
 
 
+def test_reference_arm_batch_contract():
+    """The default workload (C5 batch) on the reference arm: a thread pool over paths."""
+    d = run_bench("--impl", "reference", "--steps", "1", "--warmup", "0", "--cpu-paths", "8")
+    assert BASE_KEYS <= d.keys() and d["impl"] == "reference" and d["value"] > 0
+    assert d["config"]["workload"].startswith("batch8192") and "pool" in d["cpu_baseline"]["sample"]
+
+
+@pytest.mark.gpu
+def test_our_arm_batch_contract(gpu):
+    d = run_bench("--steps", "2", "--warmup", "1", "--no-cpu-baseline", "--paths-per-step", "512")
+    assert BASE_KEYS <= d.keys()
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 2 and d["scaling"] == "weak"
+    assert d["config"]["workload"].startswith("batch8192") and d["paths"]["tracked"] == 1024
+    assert d["gpu_launches"] == 2 and 0 < d["roofline"]["frac"] < 1
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 512 * 2 * 2 * 32 * 8
+
+
 @pytest.mark.gpu
 def test_our_arm_contract(gpu):
-    d = run_bench("--steps", "2", "--warmup", "3", "--no-cpu-baseline")
+    d = run_bench("--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--workload", "chandra64")
     assert BASE_KEYS <= d.keys()
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
     assert d["config"]["workload"] == "chandra64-dd"
