@@ -19,13 +19,18 @@ INLIB    := $(PKG)/libpt_inputs.so
 HDRS     := $(SRC)/mp.cuh $(SRC)/device.cuh $(SRC)/mgs_warp.cuh $(SRC)/plan.hpp $(SRC)/work.hpp \
             $(SRC)/kernels.cuh $(SRC)/kernel_set.hpp include/pathtrack_b200.h
 # one translation unit per precision: the three ptxas runs proceed in parallel
-KOBJS    := $(SRC)/kern_d.o $(SRC)/kern_dd.o $(SRC)/kern_qd.o $(SRC)/kern_misc.o $(SRC)/tracker.o
+KOBJS    := $(SRC)/kern_d.o $(SRC)/kern_dd.o $(SRC)/kern_dd_exact.o $(SRC)/kern_qd.o $(SRC)/kern_misc.o \
+            $(SRC)/tracker.o
 INOBJS   := $(SRC)/gen.o $(SRC)/sysio.o $(SRC)/pieri.o
 
 all: $(LIB) $(INLIB) oracle
 
 $(SRC)/%.o: $(SRC)/%.cu $(HDRS)
-	$(NVCC) $(NVFLAGS) -c $< -o $@
+	$(NVCC) $(NVFLAGS) $(KFLAGS) -c $< -o $@
+
+# the fast DD tracking kernels: dd_norm without the non-finite select (paths
+# that meet inf / NaN are re-tracked by kern_dd_exact.o, pathtrack_b200.h)
+$(SRC)/kern_dd.o: KFLAGS := -DPT_DD_FAST_NONFINITE
 
 $(SRC)/%.o: $(SRC)/%.cpp $(SRC)/mp.cuh $(SRC)/inputs.hpp include/pathtrack_inputs.h
 	$(HOSTCXX) $(HOSTFLAGS) -c $< -o $@

@@ -64,6 +64,16 @@ enum { PT_PATH_SUCCESS = 0, PT_PATH_FAIL = 1 };
 enum { PT_FAIL_NONE = 0, PT_FAIL_START = 1, PT_FAIL_MAX_STEPS = 2, PT_FAIL_MIN_STEP = 3,
        PT_FAIL_ABORT = 4 /* device watchdog: a barrier or MGS exchange stalled (not a SPEC outcome) */ };
 
+/* pt_path_stats.flags.  PT_STAT_NONFINITE: the path met a non-finite value
+ * (max|h|, max|dx| or an MGS diagonal was inf / NaN, or the end point is).
+ * DD paths are tracked by kernels whose dd_norm skips the reference's
+ * non-finite fix-up (multiprec.hpp:102-107, a select on the critical chain);
+ * they are bit-identical to the reference whenever no DD intermediate is
+ * inf / NaN, and every path that met one is re-tracked from its start by the
+ * exact kernels (same stream, no host round trip), so the reported results
+ * always follow the reference's rules. */
+enum { PT_STAT_NONFINITE = 1 };
+
 /* One polynomial system in canonical distributed form.
  * Equation i owns terms [eq_ptr[i], eq_ptr[i+1]); term t owns the
  * (var, exp) pairs [term_ptr[t], term_ptr[t+1]) with strictly increasing var
@@ -99,7 +109,7 @@ typedef struct {
   int32_t newton_iters;    /* evaluations, start validation included */
   int32_t start_iters;     /* evaluations of the t=0 start validation */
   int32_t solves;          /* completed least-squares solves (MGS + back substitution) */
-  int32_t reserved;
+  int32_t flags;           /* PT_STAT_NONFINITE: see below */
   double final_residual;   /* last max|h| computed */
   double final_update;     /* last max|dx| computed (-1 if none) */
   double t_end;            /* last accepted t */

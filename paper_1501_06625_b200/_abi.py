@@ -45,7 +45,7 @@ class PathStats(C.Structure):
         ("steps", C.c_int32),
         ("accepted", C.c_int32),
         ("newton_iters", C.c_int32),
-        ("start_iters", C.c_int32), ("solves", C.c_int32), ("reserved", C.c_int32),
+        ("start_iters", C.c_int32), ("solves", C.c_int32), ("flags", C.c_int32),
         ("final_residual", C.c_double),
         ("final_update", C.c_double),
         ("t_end", C.c_double),

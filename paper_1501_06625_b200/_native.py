@@ -14,7 +14,8 @@ from ._abi import *  # noqa: F401,F403  (structs, error codes, pointer helpers)
 from ._abi import NativeError, PathStats, StepParams, SystemDesc, TraceEvent, _dp, _vp, dptr, iptr  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpathtrack_b200.so")
+# PT_LIB_PATH: A/B experiments only (tools/); the product loads the in-tree library
+LIB_PATH = os.environ.get("PT_LIB_PATH") or os.path.join(_HERE, "libpathtrack_b200.so")
 
 
 # name -> (restype, argtypes); every symbol declared in include/pathtrack_b200.h

@@ -37,7 +37,7 @@ constexpr int kMaxDegree = 8;
 constexpr double kTimeoutNs = 20e9;
 constexpr int kMaxCols = 520;  // n + 1 <= 513 MGS columns (shared flag arrays)
 
-enum { CTL_BAR_COUNT = 0, CTL_BAR_GEN = 1, CTL_ABORT = 2, CTL_RANK = 3, CTL_QUEUE = 4, CTL_WORDS = 8 };
+enum { CTL_BAR_COUNT = 0, CTL_BAR_GEN = 1, CTL_ABORT = 2, CTL_RANK = 3, CTL_QUEUE = 4, CTL_NONFINITE = 5, CTL_WORDS = 8 };
 enum { NW_OK = 0, NW_RESIDUAL_INCREASE = 1, NW_ITERATION_BUDGET = 2, NW_LINEAR_SOLVE = 3, NW_ABORT = 4 };
 
 struct DevPlan {
@@ -913,6 +913,7 @@ __device__ __forceinline__ bool mgs_normalize(const DevPlan& P, const Work& W, c
     const double d = r_hi(rjj);
     const double mx = d > prev ? d : prev;
     ok = d > sqrt_eps * mx;
+    if (!ptk::finite(d)) atomicExch(W.ctl + CTL_NONFINITE, 1ull);  // see pt_path_stats.flags
     if (pmax_sm)
       pmax_sm[j] = mx;
     else
@@ -1302,12 +1303,13 @@ struct NewtonOut {
   int ok, kind, iters;
   double residual, update;
   int solves;
+  int nonfinite;  // max|h|, max|dx| or an MGS diagonal was inf / NaN (pt_path_stats.flags)
 };
 
 template <class R, class Team>
 __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                             const pt_step_params& sp, double t, unsigned long long& epoch) {
-  NewtonOut o{0, NW_ITERATION_BUDGET, 0, -1.0, -1.0, 0};
+  NewtonOut o{0, NW_ITERATION_BUDGET, 0, -1.0, -1.0, 0, 0};
   const double sqrt_eps = kSqrtEps<R>();
   double last = bitsd(0x7ff0000000000000ull);
   const int tid = team.block * kThreads + threadIdx.x, nth = team.nblocks * kThreads;
@@ -1323,15 +1325,16 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       xs = colsm;
     }
     eval_monomials<R>(P, W, xs, tid, nth);
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_MONO);
     eval_slots<R, Team>(P, W, team, sh, t);
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_SLOTS);
     double r = 0.0;
     for (int i = threadIdx.x; i < P.N; i += kThreads) r = nan_max(r, W.hmod[i]);
     r = block_nan_max(r, sh.red);
     o.residual = r;
+    o.nonfinite |= !ptk::finite(r);
     if (r > last) {
       o.kind = NW_RESIDUAL_INCREASE;
       return o;
@@ -1347,12 +1350,13 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       mgs_warp<R, Team>(P, W, team, sh, colsm, epoch, sqrt_eps);
     else
       mgs<R, Team>(P, W, team, sh, colsm, Team::kQInGlobal ? nullptr : sh.pmax, epoch, sqrt_eps);
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_MGS);
     if (threadIdx.x == 0) ++sh.mgs_seq;  // read again only after the next team barrier
     // a watchdog inside the MGS exchange (cluster / block teams) set CTL_ABORT
     // before its CTA arrived at the barrier above: every CTA sees it here
-    if (!Team::kGrid && ld_acquire(W.ctl + CTL_ABORT)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    if (!Team::kGrid && ld_acquire(W.ctl + CTL_ABORT)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
+    o.nonfinite |= ld_acquire(W.ctl + CTL_NONFINITE) != 0ull;
     if (ld_acquire(W.ctl + CTL_RANK) == epoch) {
       o.kind = NW_LINEAR_SOLVE;
       return o;
@@ -1366,11 +1370,12 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       const double u = backsub_update<R>(P, W, sh);
       if (threadIdx.x == 0) W.scal[0] = u;
     }
-    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0};
+    if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_BACKSUB);
     const double u = *(volatile double*)(W.scal);
     ++o.solves;
     o.update = u;
+    o.nonfinite |= !ptk::finite(u);
     if (u < sp.newton_tol) {
       o.ok = 1;
       o.kind = NW_OK;
@@ -1388,12 +1393,16 @@ struct TrackIO {
   pt_trace_event* trace;
   int trace_cap;
   int* trace_len;
+  int retrack;          // exact re-track launch: run only if stats->flags has PT_STAT_NONFINITE
 };
 
 template <class R, class Team>
 __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                            const pt_step_params& sp, const TrackIO& io, unsigned long long epoch_base) {
   const int n = P.n;
+  // exact re-track launch (DD): only paths whose fast run met a non-finite
+  // value run again; every CTA reads the same word, so all leave together
+  if (io.retrack && !(((volatile const pt_path_stats*)io.stats)->flags & PT_STAT_NONFINITE)) return;
   unsigned long long epoch = epoch_base;
   const bool leader = team.block == 0;
   pt_path_stats st{};
@@ -1416,6 +1425,7 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
   if (!team.sync(&sh.flag)) return aborted(0);
   NewtonOut o = newton<R, Team>(P, W, team, sh, colsm, sp, 0.0, epoch);
   if (o.kind == NW_ABORT) return aborted(o.iters);
+  int nonfinite = o.nonfinite;
   st.start_iters = o.iters;
   st.newton_iters = o.iters;
   st.solves = o.solves;
@@ -1453,6 +1463,7 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
       if (o.kind == NW_ABORT) return aborted(o.iters);
       st.newton_iters += o.iters;
       st.solves += o.solves;
+      nonfinite |= o.nonfinite;
       st.final_residual = o.residual;
       st.final_update = o.update;
       if (leader && threadIdx.x == 0 && io.trace && ntrace < io.trace_cap)
@@ -1491,7 +1502,15 @@ __device__ void track_path(const DevPlan& P, const Work& W, const Team& team, Sm
       for (int i = threadIdx.x; i < n; i += kThreads) store_c<R>(io.end, n, i, load_c<R>(newest, n, i));
     }
   }
+  if (leader) {  // a non-finite end point counts too (NaN-propagating check over the limbs)
+    __syncthreads();  // io.end was written with another thread-to-entry mapping
+    int bad = 0;
+    for (int q = threadIdx.x; q < 2 * limbs_of<R>::L * n; q += kThreads) bad |= !ptk::finite(io.end[q]);
+    bad = __syncthreads_or(bad);
+    nonfinite |= bad;
+  }
   if (leader && threadIdx.x == 0) {
+    st.flags = nonfinite ? PT_STAT_NONFINITE : 0;
     *io.stats = st;
     if (io.trace_len) *io.trace_len = ntrace;
   }

@@ -1,4 +1,7 @@
-// kern_dd.cu -- the tracker kernels instantiated for R = ptk::dd (see kernels.cuh).
+// kern_dd.cu -- the tracker kernels instantiated for R = ptk::dd (see kernels.cuh),
+// compiled with -DPT_DD_FAST_NONFINITE (Makefile): dd_norm without the
+// non-finite select; paths that meet a non-finite value are re-tracked by
+// kern_dd_exact.cu (pt_path_stats.flags).
 #include "kernels.cuh"
 
 const ptdev::KernelSet ptdev::kset_dd = {

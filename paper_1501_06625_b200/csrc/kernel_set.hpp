@@ -17,6 +17,8 @@ struct KernelSet {
   const void* arith;          // k_arith<R>(int op, long count, const double*, const double*, double*)
 };
 extern const KernelSet kset_d, kset_dd, kset_qd;
+// dd with the reference's non-finite rule (kern_dd_exact.cu); kset_dd is the fast set
+extern const KernelSet kset_dd_exact;
 
 struct MiscKernels {
   const void* fp64_peak;   // (double* out, int iters)

@@ -135,7 +135,7 @@ template <class R>
 __global__ void __launch_bounds__(kThreads, kBatchCtasPerSm<R>)
     k_track_batch(DevPlan P, double* dbase, unsigned long long* ubase, Layout lay, pt_step_params sp,
                   const double* starts, double* ends, pt_path_stats* stats, int n_paths,
-                  unsigned long long* queue, unsigned long long epoch_base) {
+                  unsigned long long* queue, unsigned long long epoch_base, int retrack) {
   __shared__ Smem<R> sh;
   __shared__ int s_path;
   __shared__ uint32_t s_flags[kMaxCols];
@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(kThreads, kBatchCtasPerSm<R>)
     const int p = s_path;
     __syncthreads();
     if (p >= n_paths) break;
-    TrackIO io{starts + p * PS, ends + p * PS, stats + p, nullptr, 0, nullptr};
+    // exact re-track launch: only the paths whose fast run met a non-finite value
+    if (retrack && !(((volatile const pt_path_stats*)(stats + p))->flags & PT_STAT_NONFINITE)) continue;
+    TrackIO io{starts + p * PS, ends + p * PS, stats + p, nullptr, 0, nullptr, 0};
     track_path<R, BlockTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io,
                              epoch_base + ((unsigned long long)p << 16));
     // watchdog abort (the stats of path p say PT_FAIL_ABORT): this CTA's

@@ -259,6 +259,7 @@ struct WarpMgs {
       const double d = r_hi(rjj);
       mx = d > prev ? d : prev;
       ok = d > sqrt_eps * mx;
+      if (!ptk::finite(d)) atomicExch(W.ctl + CTL_NONFINITE, 1ull);  // see pt_path_stats.flags
       if constexpr (Team::kQInGlobal)
         W.rmaxp[j] = mx;
       else

@@ -36,6 +36,9 @@ int fail(int code, const std::string& msg) {
 
 inline int limbs(pt_prec p) { return p == PT_D ? 1 : (p == PT_DD ? 2 : 4); }
 inline const KernelSet& kset(pt_prec p) { return p == PT_D ? kset_d : (p == PT_DD ? kset_dd : kset_qd); }
+// kernels that follow the reference's non-finite rules exactly: the DD set
+// differs (kset_dd skips dd_norm's non-finite select); D and QD are exact as is
+inline const KernelSet& kset_exact(pt_prec p) { return p == PT_DD ? kset_dd_exact : kset(p); }
 
 // Launch a kernel (as a cluster of `cluster` CTAs when cluster > 0) from its
 // untyped pointer.
@@ -177,7 +180,7 @@ int dispatch_grid_size(pt_plan* p) {
   want = std::max(want, (long)(p->n + 1 + gpc_mgs - 1) / gpc_mgs);
   p->grid_blocks = (int)std::min<long>(want, std::min(cap, sms));
   p->grid_dyn_smem = engine_smem(p->L, p->N, p->n, p->grid_blocks, false, &p->grid_warp);
-  for (const void* f : {fn, kset(p->prec).eval}) {
+  for (const void* f : {fn, kset_exact(p->prec).eval}) {
     rc = set_dyn_smem(f, p->grid_dyn_smem);
     if (rc) return rc;
   }
@@ -192,6 +195,7 @@ int dispatch_grid_size(pt_plan* p) {
 int setup_cluster(pt_plan* p) {
   const void* fn = kset(p->prec).track_cluster;
   PT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  PT_CUDA(cudaFuncSetAttribute(kset_exact(p->prec).track_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   p->cluster_size = 0;
   const char* ce = getenv("PT_CLUSTER_MAX");  // tuning knob: cap the cluster size
   const int cmax = ce ? atoi(ce) : 16;
@@ -259,7 +263,9 @@ int stage_fits(const pt_plan* p, size_t dyn_bytes) {
 // the monomial evaluation can read x from a shared-memory copy
 int x_fits(const pt_plan* p, size_t dyn_bytes) { return (size_t)2 * p->L * p->n * 8 <= dyn_bytes ? 1 : 0; }
 
-void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
+// One single-path launch of kernel set `ks` on the plan's engine.
+void launch_engine(pt_plan* p, const KernelSet& ks, const pt_step_params& sp, const TrackIO& io, cudaStream_t s,
+                   cudaError_t* err) {
   Work W = carve(p->dwork, p->uwork, p->lay, 0);
   unsigned long long epoch = (++p->launches) << 40;
   // barrier / abort / rank words start clean on every launch (a watchdog
@@ -269,7 +275,7 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
   // the max-dynamic-smem attribute belongs to the kernel function, not to the
   // plan: set this plan's value right before its launch (another live plan
   // of the same precision may have lowered it since)
-  const void* fn = p->engine == 1 ? kset(p->prec).track_cluster : kset(p->prec).track_grid;
+  const void* fn = p->engine == 1 ? ks.track_cluster : ks.track_grid;
   *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)std::max<size_t>(p->engine == 1 ? p->cluster_dyn_smem : p->grid_dyn_smem, 1));
   if (*err != cudaSuccess) return;
@@ -292,6 +298,16 @@ void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaSt
   dp.x_smem = x_fits(p, p->grid_dyn_smem);
   void* args[] = {&dp, &W, &spc, &ioc, &epoch};
   *err = cudaLaunchCooperativeKernel(fn, dim3(p->grid_blocks), dim3(kThreads), args, p->grid_dyn_smem, s);
+}
+
+// track_path on the device: the fast kernels, then (DD) the exact re-track
+// launch, which exits at once unless the fast run flagged PT_STAT_NONFINITE.
+void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
+  launch_engine(p, kset(p->prec), sp, io, s, err);
+  if (*err != cudaSuccess || &kset_exact(p->prec) == &kset(p->prec)) return;
+  TrackIO re = io;
+  re.retrack = 1;
+  launch_engine(p, kset_exact(p->prec), sp, re, s, err);
 }
 
 int validate_params(const pt_step_params* sp) {
@@ -634,7 +650,7 @@ int pt_track_path_device(pt_plan* p, const double* d_start, const pt_step_params
   if (rc) return rc;
   PT_CUDA(cudaSetDevice(p->device));
   cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
-  TrackIO io{d_start, d_end, d_stats, p->d_trace, p->trace_cap, p->d_trace_len};
+  TrackIO io{d_start, d_end, d_stats, p->d_trace, p->trace_cap, p->d_trace_len, 0};
   cudaError_t err = cudaSuccess;
   launch_grid(p, *sp, io, s, &err);
   if (err != cudaSuccess) return fail(PT_E_CUDA, std::string("track launch: ") + cudaGetErrorString(err));
@@ -705,8 +721,19 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   pt_step_params spc = *sp;
   int np = n_paths;
   unsigned long long ep = epoch;
-  void* args[] = {&bdp, &p->bwork, &p->bu, &lay, &spc, &d_starts, &d_ends, &d_stats, &np, &p->d_queue, &ep};
+  int retrack = 0;
+  void* args[] = {&bdp, &p->bwork, &p->bu, &lay, &spc, &d_starts, &d_ends, &d_stats, &np, &p->d_queue, &ep, &retrack};
   PT_CUDA(launch_ex(kset(p->prec).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
+  if (&kset_exact(p->prec) != &kset(p->prec)) {
+    // exact re-track of the paths whose fast run met a non-finite value
+    // (PT_STAT_NONFINITE): the queue restarts, the abort word is kept
+    PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 8, s));
+    rc = set_dyn_smem(kset_exact(p->prec).track_batch, p->batch_dyn_smem);
+    if (rc) return rc;
+    retrack = 1;
+    ep = (++p->launches) << 40;
+    PT_CUDA(launch_ex(kset_exact(p->prec).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
+  }
   PT_CUDA(cudaGetLastError());
   return PT_OK;
 }
@@ -759,7 +786,7 @@ int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J
   dp.mgs_smem = 0;
   dp.mgs_warp = 0;
   void* args[] = {&dp, &W, &dx, &t, &dh, &dJ, &dr};
-  const void* fn = kset(p->prec).eval;
+  const void* fn = kset_exact(p->prec).eval;
   rc = set_dyn_smem(fn, p->grid_dyn_smem);
   if (rc) return rc;
   PT_CUDA(cudaMemset(W.ctl, 0, CTL_WORDS * sizeof(unsigned long long)));
@@ -790,7 +817,7 @@ int pt_eval_bench(pt_plan* p, const double* x, double t, int32_t reps, double* m
   dp.mgs_warp = 0;
   double* null = nullptr;
   void* args[] = {&dp, &W, &dx, &t, &null, &null, &null};
-  const void* fn = kset(p->prec).eval;
+  const void* fn = kset_exact(p->prec).eval;
   rc = set_dyn_smem(fn, p->grid_dyn_smem);
   if (rc) return rc;
   PT_CUDA(cudaMemset(W.ctl, 0, CTL_WORDS * sizeof(unsigned long long)));
@@ -846,7 +873,7 @@ int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, co
     dp.mgs_gw = ptplan::mgs_group_warps(N);
     const int gpc = kWarps / dp.mgs_gw;
     int per_sm = 0, sms = 0;
-    const void* fn = kset(prec).lstsq;
+    const void* fn = kset_exact(prec).lstsq;
     rc = occupancy_blocks(fn, device, &per_sm, &sms);
     if (rc) return rc;
     int blocks = std::min(std::min(sms, std::max(1, per_sm) * sms), std::max(1, (n + 1 + gpc - 1) / gpc));
@@ -903,7 +930,7 @@ int pt_arith_device(int device, pt_prec prec, int32_t op, int64_t count, const d
   long cnt = (long)count;
   int opc = op;
   void* args[] = {&opc, &cnt, &da, &db, &dout};
-  PT_CUDA(cudaLaunchKernel(kset(prec).arith, dim3(blocks), dim3(256), args, 0, 0));
+  PT_CUDA(cudaLaunchKernel(kset_exact(prec).arith, dim3(blocks), dim3(256), args, 0, 0));
   PT_CUDA(cudaGetLastError());
   PT_CUDA(cudaDeviceSynchronize());
   PT_CUDA(cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost));

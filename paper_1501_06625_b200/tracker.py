@@ -62,12 +62,14 @@ class TrackOutcome:
     failure_kind: str
     trace: List[nat.TraceEvent] = field(default_factory=list)
     solves: int = 0  # completed least-squares solves
+    flags: int = 0   # PT_STAT_NONFINITE (1): met inf / NaN, re-tracked by the exact DD kernels
 
     @staticmethod
     def from_native(end: np.ndarray, st: nat.PathStats, trace=None) -> "TrackOutcome":
         return TrackOutcome(st.status == 0, end, st.steps, st.accepted, st.newton_iters, st.start_iters,
                             st.final_residual, st.final_update, st.t_end,
-                            FAILURE_KINDS.get(st.failure_kind, str(st.failure_kind)), trace or [], st.solves)
+                            FAILURE_KINDS.get(st.failure_kind, str(st.failure_kind)), trace or [], st.solves,
+                            st.flags)
 
 
 class Homotopy:

@@ -161,3 +161,51 @@ def test_large_plan_survives_a_smaller_plan(gpu, orc):
         assert_bits_equal_nan(out.end, end_ref, "end point after a smaller plan")
     _, outs = hb.track_batch(np.repeat(big.starts, 2, axis=0), big.params)
     assert all(o.success for o in outs)
+
+
+# ---- non-finite values: the exact DD re-track (pathtrack_b200.h PT_STAT_NONFINITE) ----
+def _overflow_homotopy(prec):
+    """f = 1e308 x^2 + 1e308 x - 3 overflows at x = 1 (not at x = 0.001);
+    g = (x - 1)(x - 0.001) has both as start roots."""
+    f = pt.PolynomialSystem.from_terms(1, [[([], -3.0), ([(0, 1)], 1e308), ([(0, 2)], 1e308)]], prec)
+    g = pt.PolynomialSystem.from_terms(1, [[([], 0.001), ([(0, 1)], -1.001), ([(0, 2)], 1.0)]], prec)
+    starts = np.stack([pt.limbs_from_complex([v], prec) for v in (1.0, 0.001, 1.0, 0.001, 1.0)])
+    return g, f, pt.gamma_from_seed(5, prec), starts
+
+
+@pytest.mark.parametrize("engine", ["grid", "cluster"])
+def test_nonfinite_path_is_retracked_exactly(gpu, orc, engine):
+    """A DD path that meets inf / NaN is flagged by the fast kernels and
+    re-tracked by the exact ones: its results follow the reference's
+    non-finite rules (multiprec.hpp:102-107) bit for bit (NaN payloads aside)."""
+    prec = PM.DD
+    g, f, gamma, starts = _overflow_homotopy(prec)
+    params = pt.StepControlParams.defaults(prec)
+    hom = pt.make_homotopy(g, f, gamma, 2, device=gpu)
+    hom.set_engine(engine)
+    for p in (0, 1):
+        out = hom.track_path(starts[p], params, trace=True)
+        ref = orc.track_path(int(prec), g, f, gamma, 2, starts[p], params, params.max_steps + 2)
+        _compare_track(out, *ref)
+        assert bool(out.flags & 1) == (p == 0), (p, out.flags)
+
+
+def test_nonfinite_paths_in_a_batch(gpu, orc):
+    prec = PM.DD
+    g, f, gamma, starts = _overflow_homotopy(prec)
+    params = pt.StepControlParams.defaults(prec)
+    hom = pt.make_homotopy(g, f, gamma, 2, device=gpu)
+    ends, outs = hom.track_batch(starts, params)
+    ends_ref, st_ref = orc.track_batch(int(prec), g, f, gamma, 2, starts, params, 2)
+    for p, (o, s) in enumerate(zip(outs, st_ref)):
+        assert (o.success, o.steps, o.newton_iters, o.solves) == (s.status == 0, s.steps, s.newton_iters, s.solves)
+        assert_bits_equal_nan(np.array([o.final_residual, o.final_update, o.t_end]),
+                              np.array([s.final_residual, s.final_update, s.t_end]), f"stats {p}")
+        assert bool(o.flags & 1) == (p % 2 == 0)
+    assert_bits_equal_nan(ends, ends_ref, "ends")
+
+
+def test_finite_paths_are_not_flagged(gpu):
+    w = W.chandra(64, PM.DD)
+    hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)
+    assert hom.track_path(w.start, w.params).flags == 0
