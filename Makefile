@@ -16,10 +16,10 @@ PKG      := paper_1501_06625_b200
 SRC      := $(PKG)/csrc
 LIB      := $(PKG)/libpathtrack_b200.so
 INLIB    := $(PKG)/libpt_inputs.so
-HDRS     := $(SRC)/mp.cuh $(SRC)/device.cuh $(SRC)/mgs_warp.cuh $(SRC)/plan.hpp $(SRC)/work.hpp \
+HDRS     := $(SRC)/mp.cuh $(SRC)/mp_qdfast.cuh $(SRC)/mgs_batch.cuh $(SRC)/device.cuh $(SRC)/mgs_warp.cuh $(SRC)/plan.hpp $(SRC)/work.hpp \
             $(SRC)/kernels.cuh $(SRC)/kernel_set.hpp include/pathtrack_b200.h
 # one translation unit per precision: the three ptxas runs proceed in parallel
-KOBJS    := $(SRC)/kern_d.o $(SRC)/kern_dd.o $(SRC)/kern_dd_exact.o $(SRC)/kern_qd.o $(SRC)/kern_misc.o \
+KOBJS    := $(SRC)/kern_d.o $(SRC)/kern_dd.o $(SRC)/kern_dd_exact.o $(SRC)/kern_qd.o $(SRC)/kern_qd_fast.o $(SRC)/kern_misc.o \
             $(SRC)/tracker.o
 INOBJS   := $(SRC)/gen.o $(SRC)/sysio.o $(SRC)/pieri.o
 
@@ -31,6 +31,8 @@ $(SRC)/%.o: $(SRC)/%.cu $(HDRS)
 # the fast DD tracking kernels: dd_norm without the non-finite select (paths
 # that meet inf / NaN are re-tracked by kern_dd_exact.o, pathtrack_b200.h)
 $(SRC)/kern_dd.o: KFLAGS := -DPT_DD_FAST_NONFINITE
+# the tolerance-parity QD kernels (mp_qdfast.cuh, pt_plan_set_arith)
+$(SRC)/kern_qd_fast.o: KFLAGS := -DPT_QD_FAST
 
 $(SRC)/%.o: $(SRC)/%.cpp $(SRC)/mp.cuh $(SRC)/inputs.hpp include/pathtrack_inputs.h
 	$(HOSTCXX) $(HOSTFLAGS) -c $< -o $@

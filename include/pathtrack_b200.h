@@ -149,6 +149,19 @@ int64_t pt_plan_info(const pt_plan* plan, int32_t what);
  * produce bit-identical results. */
 int pt_plan_set_engine(pt_plan* plan, int32_t engine);
 
+/* Arithmetic of a QD plan's tracking kernels.  PT_ARITH_REFERENCE (default):
+ * the reference operation sequences (multiprec.hpp), bit-identical to the
+ * reference tracker.  PT_ARITH_FAST: tolerance parity -- classic quad-double
+ * algorithms (sloppy add, truncated product, long division) and a
+ * reciprocal-square-root MGS normalisation (no division on the column chain);
+ * end points agree with the reference to ~1e-60 relative (scaled by the
+ * conditioning), step / Newton counts agree barring ties at the step-control
+ * thresholds.  D and DD plans accept only
+ * PT_ARITH_REFERENCE.  Applies to pt_track_path / pt_track_batch /
+ * pt_eval_homotopy of this plan. */
+enum { PT_ARITH_REFERENCE = 0, PT_ARITH_FAST = 1 };
+int pt_plan_set_arith(pt_plan* plan, int32_t arith);
+
 /* Algorithmic work of one unit of the path, counted on the reference
  * algorithms.  kind: 0 one evaluation (h and J),
  * 1 one least-squares solve + update, 2 one prediction of degree `degree`.
@@ -221,6 +234,9 @@ int pt_lstsq(int device, pt_prec prec, int32_t N, int32_t n, const double* A, co
  * op codes and element layout as documented in DESIGN.md section 3. */
 int pt_arith_device(int device, pt_prec prec, int32_t op, int64_t count, const double* a, const double* b,
                     double* out);
+/* The same with an explicit arithmetic (PT_ARITH_FAST: the fast QD set). */
+int pt_arith_device_mode(int device, pt_prec prec, int32_t arith, int32_t op, int64_t count, const double* a,
+                         const double* b, double* out);
 /* The same operations through the host build of the device arithmetic. */
 int pt_arith_host(pt_prec prec, int32_t op, int64_t count, const double* a, const double* b, double* out);
 

@@ -27,6 +27,7 @@ PROTOTYPES = {
     "pt_plan_destroy": (None, [_vp]),
     "pt_plan_info": (C.c_int64, [_vp, C.c_int32]),
     "pt_plan_set_engine": (C.c_int, [_vp, C.c_int32]),
+    "pt_plan_set_arith": (C.c_int, [_vp, C.c_int32]),
     "pt_plan_set_trace": (C.c_int, [_vp, C.c_int32]),
     "pt_plan_work": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
     "pt_fp64_peak": (C.c_int, [C.c_int, _dp, _dp]),
@@ -43,6 +44,7 @@ PROTOTYPES = {
     "pt_eval_bench": (C.c_int, [_vp, _dp, C.c_double, C.c_int32, _dp]),
     "pt_lstsq": (C.c_int, [C.c_int, C.c_int, C.c_int32, C.c_int32, _dp, _dp, _dp]),
     "pt_arith_device": (C.c_int, [C.c_int, C.c_int, C.c_int32, C.c_int64, _dp, _dp, _dp]),
+    "pt_arith_device_mode": (C.c_int, [C.c_int, C.c_int, C.c_int32, C.c_int32, C.c_int64, _dp, _dp, _dp]),
     "pt_arith_host": (C.c_int, [C.c_int, C.c_int32, C.c_int64, _dp, _dp, _dp]),
     "pt_last_error": (C.c_char_p, []),
     "pt_version": (C.c_char_p, []),

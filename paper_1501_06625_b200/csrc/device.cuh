@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "../../include/pathtrack_b200.h"
 #include "mp.cuh"
@@ -65,6 +66,15 @@ struct DevPlan {
   int mgs_B;     // warp MGS: consecutive columns per CTA block (divides kWarps)
   int bs_smem;   // warp back substitution stages R in CTA 0's dynamic shared memory
   int x_smem;    // monomial evaluation reads x from a per-CTA shared-memory copy
+  int mgs_batch; // batch (BlockTeam, N <= 64): column-item MGS on a padded shared-memory matrix (mgs_batch)
+  // batch only (BlockTeam): lane tasks as warp bundles over lane-interleaved
+  // contribution streams (plan.hpp Bundle); bundles == nullptr: unbundled
+  const ptplan::Bundle* bundles;
+  int bundle_warp_beg[kWarps + 1];
+  const ptplan::SlotTask* btasks;
+  const int32_t* s_ws;
+  const double* s_coef;
+  long s_len;
 };
 
 // One path's workspace.  All arrays are complex SoA unless noted.
@@ -653,22 +663,10 @@ __device__ __forceinline__ cplx<R> slot_sum(const DevPlan& P, const Work& W, con
   return group_tree(acc, g, Pw, K, sm);
 }
 
-// Canonical width-32 sum of K <= 512 contributions by ONE lane (lane tasks).
-// Leaves are the partials p = c[p] + c[p+32] + ... (each summed in order);
-// visiting them in 5-bit bit-reversed order p = brev(t) and merging the two
-// top entries of a small stack after every leaf whose count t+1 is a multiple
-// of 2, 4, ... reproduces the tree exactly: the first merges are
-// (c0 + c16), (c8 + c24), then (c0+c16) + (c8+c24) = level 8, and so on, each
-// merge being partial[p] += partial[p+off] with the lower index on the left.
-// An empty right subtree (its least index p+off >= K) is skipped, exactly the
-// "p + off < K" rule.  Stack positions depend only on t: fully unrolled, the
-// stack lives in registers.  No shuffles, no idle lanes.
-__host__ __device__ constexpr int brev5(int t) {
-  return ((t & 1) << 4) | ((t & 2) << 2) | (t & 4) | ((t & 8) >> 2) | ((t & 16) >> 4);
-}
-__host__ __device__ constexpr int popc5(int t) { return (t & 1) + ((t >> 1) & 1) + ((t >> 2) & 1) + ((t >> 3) & 1) + ((t >> 4) & 1); }
-__host__ __device__ constexpr int ctz6(int x) { return (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : (x & 8) ? 3 : (x & 16) ? 4 : 5; }
-
+// Canonical width-32 sums of K <= 512 contributions by ONE lane (lane tasks):
+// leaves are the partials p = c[p] + c[p+32] + ... (each summed in order),
+// merged by the levels off = 16 .. 1, an empty right subtree (least index
+// p + off >= K) skipped.  No shuffles, no idle lanes.
 // K <= KMAX: all contributions in registers, levels off = 4, 2, 1 only.
 template <class R, int KMAX>
 __device__ __forceinline__ cplx<R> lane_sum(const DevPlan& P, const Work& W, int beg, int K) {
@@ -686,31 +684,86 @@ __device__ __forceinline__ cplx<R> lane_sum(const DevPlan& P, const Work& W, int
   return part[0];
 }
 
-template <class R>
-__device__ __forceinline__ cplx<R> lane_canon32(const DevPlan& P, const Work& W, int beg, int K) {
-  cplx<R> st[6];
-  bool ne[6];
+// K > KMAX: the tree rolled (code size: a fully unrolled 32-leaf tree of
+// complex DD products is ~10k instructions per copy and thrashed the
+// instruction cache of the batch kernel -- ncu: 26 % of its stall samples
+// were no_instruction).  The width-32 canonical tree splits into the
+// subtrees Q(c) of the leaves = c mod 8,
+//   Q(c) = (L_c + L_{c+16}) + (L_{c+8} + L_{c+24})       (levels off = 16, 8)
+// merged by the levels off = 4, 2, 1:
+//   ((Q0 + Q4) + (Q2 + Q6)) + ((Q1 + Q5) + (Q3 + Q7)).
+// Iteration u = 0..7 computes Q(brev3(u)) (four independent leaf sums, the
+// ILP of the body) and folds it into a three-level stack; a merge whose right
+// subtree starts at a leaf index >= K is skipped ("p + off < K").  The loop
+// structure is warp-uniform (u), only the K tests are per lane.
+__host__ __device__ constexpr int brev3(int u) { return ((u & 1) << 2) | (u & 2) | ((u & 4) >> 2); }
+
+template <class R, class Get>
+__device__ __forceinline__ cplx<R> lane_canon32_g(int K, const Get& get) {
+  cplx<R> A = c_zero<R>(), B = c_zero<R>(), C = c_zero<R>();
+#pragma unroll 1
+  for (int u = 0; u < 8; ++u) {
+    const int c = brev3(u);
+    cplx<R> q = c_zero<R>();
+    if (c < K) {  // Q(c) exists: leaves c + 8m, m = 0..3, summed round by round (c[p], c[p+32], ...)
+      cplx<R> l[4] = {c_zero<R>(), c_zero<R>(), c_zero<R>(), c_zero<R>()};
+#pragma unroll 1
+      for (int r0 = 0; r0 < K; r0 += 32) {
 #pragma unroll
-  for (int t = 0; t < 32; ++t) {
-    const int p = brev5(t);
-    const int d = popc5(t);  // stack depth before this leaf
-    cplx<R> v = c_zero<R>();
-    const bool has = p < K;
-    if (has) {
-      v = contrib<R>(P, W, P.ctr_coef[beg + p], P.ctr_ws[beg + p]);
-      for (int r = p + 32; r < K; r += 32) v = c_add(v, contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]));
+        for (int m = 0; m < 4; ++m) {
+          const int p = c + 8 * m + r0;
+          if (p < K) {
+            const cplx<R> v = get(p);
+            l[m] = r0 == 0 ? v : c_add(l[m], v);
+          }
+        }
+      }
+      cplx<R> x = l[0], y = l[1];
+      if (c + 16 < K) x = c_add(x, l[2]);  // off = 16
+      if (c + 24 < K) y = c_add(y, l[3]);
+      q = c + 8 < K ? c_add(x, y) : x;     // off = 8
     }
-    st[d] = v;
-    ne[d] = has;
-    // merges after leaf t: as many as trailing zeros of t + 1
-#pragma unroll
-    for (int m = 0; m < ctz6(t + 1); ++m) {
-      const int top = d - m;
-      if (ne[top]) st[top - 1] = c_add(st[top - 1], st[top]);
+    if ((u & 1) == 0) {
+      A = q;
+    } else {
+      if (c < K) A = c_add(A, q);  // level 4: right subtree {c}
+      if ((u & 2) == 0) {
+        B = A;
+      } else {
+        if (brev3(u - 1) < K) B = c_add(B, A);  // level 2
+        if ((u & 4) == 0)
+          C = B;
+        else if (brev3(u - 3) < K)
+          C = c_add(C, B);  // level 1
+      }
     }
   }
-  return st[0];
+  return C;
 }
+
+template <class R>
+__device__ __forceinline__ cplx<R> lane_canon32(const DevPlan& P, const Work& W, int beg, int K) {
+  return lane_canon32_g<R>(K, [&](int r) { return contrib<R>(P, W, P.ctr_coef[beg + r], P.ctr_ws[beg + r]); });
+}
+
+// Contribution streams of the batch bundles (plan.hpp Bundle): entry `at`
+// = pos*32 + lane.  The index and the 2L coefficient limbs are coalesced
+// across the warp; the workspace entry is the same for every lane when the
+// bundle's slots share their support (a broadcast).
+template <class R>
+__device__ __forceinline__ cplx<R> s_contrib(const DevPlan& P, const Work& W, long at) {
+  const int wi = P.s_ws[at];
+  const cplx<R> c = load_c<R>(P.s_coef, P.s_len * 32, at);
+  const cplx<R> m = load_c<R>(W.ws, P.ws_len, wi < 0 ? 0 : wi);
+  return pick(wi < 0, c, c_mul(c, m));
+}
+
+// lane_canon32 over a stream (contribution r of this lane at (s0 + r)*32 + lane).
+template <class R>
+__device__ __forceinline__ cplx<R> lane_canon32_s(const DevPlan& P, const Work& W, long s0, int lane, int K) {
+  return lane_canon32_g<R>(K, [&](int r) { return s_contrib<R>(P, W, (s0 + r) * 32 + lane); });
+}
+
 
 template <class R>
 __device__ __forceinline__ void slot_store(const DevPlan& P, const Work& W, const ptplan::SlotTask& tk,
@@ -731,13 +784,47 @@ __device__ __forceinline__ void slot_store(const DevPlan& P, const Work& W, cons
   }
 }
 
+// The batch's lane tasks: warp w runs its bundles (plan.hpp Bundle), lane l
+// the l-th slot of each.  Own register-allocation unit (the unrolled trees).
+template <class R>
+__device__ __noinline__ void eval_bundles(const DevPlan& P, const Work& W, const cplx<R> wS, const R wT) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = P.bundle_warp_beg[warp]; b < P.bundle_warp_beg[warp + 1]; ++b) {
+    const ptplan::Bundle B = P.bundles[b];
+    if (lane < B.ntasks) {
+      const ptplan::SlotTask tk = P.btasks[B.task_beg + lane];
+      cplx<R> Sg = c_zero<R>(), Sf = c_zero<R>();
+#pragma unroll 1
+      for (int side = 0; side < 2; ++side) {  // one copy of the tree for g and f (instruction cache)
+        const int K = side ? tk.f_cnt : tk.g_cnt;
+        const cplx<R> v = lane_canon32_s<R>(P, W, side ? B.sf : B.sg, lane, K);
+        if (side)
+          Sf = v;
+        else
+          Sg = v;
+      }
+      bool have_f;
+      if (tk.f_cnt < 0) {
+        Sf = Sg;
+        have_f = tk.g_cnt > 0;
+      } else {
+        have_f = tk.f_cnt > 0;
+      }
+      slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);
+    }
+  }
+}
+
 template <class R, class Team>
 __device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double t) {
+  __syncwarp();  // whole warps call this: converged entry (no WARPSYNC.COLLECTIVE fallback for its shuffles)
   cplx<R> wS;
   R wT;
   weights<R>(P, t, wS, wT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {  // lane tasks: one slot per lane (canonical width 32, K <= lane_k)
+  if (P.bundles != nullptr) {  // batch: lane tasks in warp bundles over coalesced streams
+    eval_bundles<R>(P, W, wS, wT);
+  } else {  // lane tasks: one slot per lane (canonical width 32, K <= lane_k)
     constexpr int KM = limbs_of<R>::L == 4 ? 4 : 8;
     const int beg = P.class_beg[0], end = P.class_beg[1];
     const int nth = team.nblocks * kThreads;
@@ -757,7 +844,8 @@ __device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const T
       slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);
     }
   }
-  for (int c = 0; c < 4; ++c) {
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {  // rolled: one copy of the group sums (instruction cache)
     const int gw = 8 >> c;
     const int gpc = kWarps / gw;
     const int gi = warp / gw;
@@ -909,7 +997,8 @@ __device__ __forceinline__ bool mgs_normalize(const DevPlan& P, const Work& W, c
   int ok = 0;
   R inv = rconst<R>(0.0);
   if (g.p == 0) {
-    const R rjj = r_sqrt(nrm2);
+    R rjj, inv1;
+    r_sqrt_inv(nrm2, rjj, inv1);
     const double d = r_hi(rjj);
     const double mx = d > prev ? d : prev;
     ok = d > sqrt_eps * mx;
@@ -919,7 +1008,7 @@ __device__ __forceinline__ bool mgs_normalize(const DevPlan& P, const Work& W, c
     else
       W.rmaxp[j] = mx;
     if (ok) {
-      inv = r_div(rconst<R>(1.0), rjj);
+      inv = inv1;
       store_r<R>(c.inv, c.inv_S, c.inv_i, inv);
       store_c<R>(c.r.p, c.r.S, j, cplx<R>{rjj, rconst<R>(0.0)});
     }
@@ -1115,6 +1204,7 @@ __device__ __forceinline__ void mgs_run(const DevPlan& P, const Work& W, const T
 template <class R, class Team>
 __device__ __noinline__ void mgs(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                                  double* pmax_sm, unsigned long long epoch, double sqrt_eps) {
+  __syncwarp();  // whole warps call this: converged entry (no WARPSYNC.COLLECTIVE fallback for its shuffles)
   if (colsm)
     mgs_run<R, Team, true>(P, W, team, sh, colsm, pmax_sm, epoch, sqrt_eps);
   else
@@ -1133,6 +1223,7 @@ __device__ __noinline__ void mgs(const DevPlan& P, const Work& W, const Team& te
 // both threads of a pair run one instruction stream.
 template <class R>
 __device__ __noinline__ double backsub_split(const DevPlan& P, const Work& W, Smem<R>& sh) {
+  __syncwarp();  // whole warps call this: converged entry (no WARPSYNC.COLLECTIVE fallback for its shuffles)
   constexpr int L = limbs_of<R>::L;
   const int n = P.n;
   const long SR = (long)n * (n + 1);
@@ -1184,6 +1275,7 @@ __device__ __noinline__ double backsub_split(const DevPlan& P, const Work& W, Sm
 
 template <class R>
 __device__ __noinline__ double backsub_update(const DevPlan& P, const Work& W, Smem<R>& sh) {
+  __syncwarp();  // whole warps call this: converged entry (no WARPSYNC.COLLECTIVE fallback for its shuffles)
   if (P.n <= kThreads / 2) return backsub_split<R>(P, W, sh);
   const int n = P.n;
   const long SR = (long)n * (n + 1);
@@ -1238,6 +1330,7 @@ __device__ __noinline__ double backsub_update(const DevPlan& P, const Work& W, S
 }  // namespace ptdev
 
 #include "mgs_warp.cuh"
+#include "mgs_batch.cuh"
 
 namespace ptdev {
 
@@ -1346,10 +1439,13 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
     }
     ++epoch;
     pc.lap(W.prof + PROF_SLOTS);
-    if (P.mgs_warp)
+    if (P.mgs_batch) {  // set for the batch kernel (BlockTeam) only
+      if constexpr (std::is_same<Team, BlockTeam>::value) mgs_batch<R>(P, W, colsm, epoch, sqrt_eps);
+    } else if (P.mgs_warp) {
       mgs_warp<R, Team>(P, W, team, sh, colsm, epoch, sqrt_eps);
-    else
+    } else {
       mgs<R, Team>(P, W, team, sh, colsm, Team::kQInGlobal ? nullptr : sh.pmax, epoch, sqrt_eps);
+    }
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_MGS);
     if (threadIdx.x == 0) ++sh.mgs_seq;  // read again only after the next team barrier
@@ -1361,7 +1457,7 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       o.kind = NW_LINEAR_SOLVE;
       return o;
     }
-    if (P.mgs_warp) {
+    if (P.mgs_warp || P.mgs_batch) {
       if (team.block == 0) {
         const double u = backsub_warp<R>(P, W, P.bs_smem ? colsm : nullptr, sh);
         if (threadIdx.x == 0) W.scal[0] = u;

@@ -19,6 +19,8 @@ struct KernelSet {
 extern const KernelSet kset_d, kset_dd, kset_qd;
 // dd with the reference's non-finite rule (kern_dd_exact.cu); kset_dd is the fast set
 extern const KernelSet kset_dd_exact;
+// qd in the tolerance-parity arithmetic (kern_qd_fast.cu, mp_qdfast.cuh)
+extern const KernelSet kset_qd_fast;
 
 struct MiscKernels {
   const void* fp64_peak;   // (double* out, int iters)

@@ -76,6 +76,18 @@ __host__ __device__ inline Work carve(double* dbase, unsigned long long* ubase, 
   return W;
 }
 
+// kern_dd.cu (-DPT_DD_FAST_NONFINITE) and kern_dd_exact.cu instantiate the same
+// templates with different device bodies: the kernels live in an inline
+// namespace per variant, so the two host stubs are distinct symbols (one
+// weak symbol would silently serve both kernel sets).
+#if defined(PT_DD_FAST_NONFINITE)
+#define PT_KVARIANT kv_fastnf
+#elif defined(PT_QD_FAST)
+#define PT_KVARIANT kv_qdfast
+#else
+#define PT_KVARIANT kv_exact
+#endif
+inline namespace PT_KVARIANT {
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
@@ -275,4 +287,5 @@ __global__ void k_arith(int op, long count, const double* a, const double* b, do
     arith_one<R>(op, a + i * 2 * L, b + i * 2 * L, out + i * 2 * L);
 }
 
+}  // inline namespace PT_KVARIANT
 }  // namespace ptdev

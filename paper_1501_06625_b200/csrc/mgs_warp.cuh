@@ -255,7 +255,8 @@ struct WarpMgs {
     R inv = rconst<R>(0.0);
     double mx = 0.0;
     if (lane == 0) {
-      const R rjj = r_sqrt(nrm2);
+      R rjj;
+      r_sqrt_inv(nrm2, rjj, inv);
       const double d = r_hi(rjj);
       mx = d > prev ? d : prev;
       ok = d > sqrt_eps * mx;
@@ -264,7 +265,6 @@ struct WarpMgs {
         W.rmaxp[j] = mx;
       else
         sh.pmax[j] = mx;
-      inv = r_div(rconst<R>(1.0), rjj);
       if (ok) {
         store_r<R>(W.inv, n, j, inv);
         store_c<R>(W.Rm, SR, (long)j * n + j, cplx<R>{rjj, rconst<R>(0.0)});
@@ -476,6 +476,7 @@ struct WarpMgs {
 template <class R, class Team, int E>
 __device__ PT_MGS_WARP_INLINE void mgs_warp_e(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double* colsm,
                                         unsigned long long epoch, double sqrt_eps) {
+  __syncwarp();  // whole warps call this: converged entry (no WARPSYNC.COLLECTIVE fallback for its shuffles)
   constexpr int L = limbs_of<R>::L;
   double* qb = colsm + mgs_warp_slots_doubles(L, P.N, P.n, team.nblocks);
   uint64_t* bb = reinterpret_cast<uint64_t*>(qb + (long)P.n * mgs_warp_qs(L, P.N));
@@ -510,6 +511,7 @@ __device__ __forceinline__ void mgs_warp(const DevPlan& P, const Work& W, const 
 template <class R>
 __device__ __noinline__ double backsub_blocked(const DevPlan& P, const Work& W, const double* Rs, const double* invs,
                                                Smem<R>& sh, cplx<R>* xs) {
+  __syncwarp();  // whole warps call this: converged entry (no WARPSYNC.COLLECTIVE fallback for its shuffles)
   const int n = P.n, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long SR = (long)n * (n + 1);
   const int nb = (n + 31) >> 5;

@@ -41,6 +41,14 @@
 #define PT_QDOP inline
 #endif
 
+// Tolerance-parity QD mode (mp_qdfast.cuh): device code of kern_qd_fast.cu,
+// or host code built with -DPT_QD_FAST_HOST (CPU accuracy tests only).
+#if defined(PT_QD_FAST) && (defined(__CUDA_ARCH__) || defined(PT_QD_FAST_HOST))
+#define PT_QD_FAST_ON 1
+#else
+#define PT_QD_FAST_ON 0
+#endif
+
 namespace ptk {
 
 #if defined(PT_COUNT_FP64) && !defined(__CUDA_ARCH__)
@@ -330,6 +338,10 @@ PT_HD void r_set_limb(dd& a, int l, double v) {
     a.lo = v;
 }
 
+}  // namespace ptk
+#include "mp_qdfast.cuh"
+namespace ptk {
+
 // ----- quad-double (multiprec.hpp:196-372) -----
 // qd_renorm5, multiprec.hpp:209-250.  Branch structure kept verbatim: the
 // zero tests decide which limbs absorb the tail, and changing them changes bits.
@@ -511,11 +523,17 @@ PT_HD void oe_sort(double (&g)[G]) {
 PT_HD qd r_from(double x, qd*) { return {{x, 0.0, 0.0, 0.0}}; }
 PT_HD qd r_neg(const qd& a) { return {{-a.c[0], -a.c[1], -a.c[2], -a.c[3]}}; }
 PT_QDOP qd r_add(qd a, qd b) {  // multiprec.hpp:290-293
+#if PT_QD_FAST_ON
+  return qdfast::add(a, b);
+#endif
   double m[8] = {a.c[0], a.c[1], a.c[2], a.c[3], b.c[0], b.c[1], b.c[2], b.c[3]};
   return qd_distill<8>(m);
 }
 PT_HD qd r_sub(qd a, qd b) { return r_add(a, r_neg(b)); }
 PT_QDOP qd r_mul(qd a, qd b) {  // multiprec.hpp:297-312
+#if PT_QD_FAST_ON
+  return qdfast::mul(a, b);
+#endif
   double m[23];
   int k = 0;
 #pragma unroll
@@ -573,6 +591,9 @@ PT_QDOP qd r_mul(qd a, qd b) {  // multiprec.hpp:297-312
   return qd_distill<23>(m);
 }
 PT_QDOP qd r_mul_d(qd a, double b) {  // multiprec.hpp:314-323
+#if PT_QD_FAST_ON
+  return qdfast::mul_d(a, b);
+#endif
   double m[8];
 #pragma unroll
   for (int i = 0; i <= 3; ++i) {
@@ -606,6 +627,9 @@ PT_QDOP qd r_mul_d(qd a, double b) {  // multiprec.hpp:314-323
   return qd_distill<8>(m);
 }
 PT_QDOP qd r_div(qd a, qd b) {  // multiprec.hpp:327-337
+#if PT_QD_FAST_ON
+  return qdfast::div(a, b);
+#endif
   double q0 = div64(a.c[0], b.c[0]);
   if (!finite(q0)) return {{q0, 0.0, 0.0, 0.0}};
   double q[5];
@@ -621,6 +645,9 @@ PT_QDOP qd r_div(qd a, qd b) {  // multiprec.hpp:327-337
   return qd_distill<5>(q);
 }
 PT_QDOP qd r_sqrt(qd a) {  // multiprec.hpp:364-372
+#if PT_QD_FAST_ON
+  return qdfast::sqrt(a);
+#endif
   if (a.c[0] == 0.0 && a.c[1] == 0.0 && a.c[2] == 0.0 && a.c[3] == 0.0) return {{0.0, 0.0, 0.0, 0.0}};
   if (a.c[0] < 0.0) return {{bitsd(0x7ff8000000000000ull), 0.0, 0.0, 0.0}};
   qd x{{div64(1.0, sqrt64(a.c[0])), 0.0, 0.0, 0.0}};
@@ -634,6 +661,9 @@ PT_HD bool r_is_zero(const qd& a) { return a.c[0] == 0.0 && a.c[1] == 0.0 && a.c
 PT_HD double r_limb(const qd& a, int l) { return a.c[l]; }
 PT_HD void r_set_limb(qd& a, int l, double v) { a.c[l] = v; }
 PT_QDOP qd qd_renormalize(qd a) {  // multiprec.hpp:283-286
+#if PT_QD_FAST_ON
+  return qdfast::renorm4(a.c[0], a.c[1], a.c[2], a.c[3]);
+#endif
   double m[4] = {a.c[0], a.c[1], a.c[2], a.c[3]};
   return qd_distill<4>(m);
 }
@@ -642,6 +672,29 @@ template <class R>
 PT_HD R rconst(double x) {
   return r_from(x, static_cast<R*>(nullptr));
 }
+
+// r = sqrt(x) and inv = 1/r, the pair every MGS normalisation needs
+// (r_kk = sqrt(norm^2), q_k = a_k * (1/r_kk)).  Reference
+// sequence: sqrt, then one division.  Fast QD mode: one reciprocal square
+// root y ~ 1/sqrt(x) (mp_qdfast.cuh) gives both, r = x y and inv = y -- no
+// division on the column chain (tolerance parity).
+template <class R>
+PT_HD void r_sqrt_inv(const R& x, R& r, R& inv) {
+  r = r_sqrt(x);
+  inv = r_div(rconst<R>(1.0), r);
+}
+#if PT_QD_FAST_ON
+template <>
+PT_HD void r_sqrt_inv<qd>(const qd& x, qd& r, qd& inv) {
+  if (!(x.c[0] > 0.0) || !finite(x.c[0])) {  // zero, negative, NaN, inf: the plain forms
+    r = r_sqrt(x);
+    inv = r_div(rconst<qd>(1.0), r);
+    return;
+  }
+  inv = qdfast::rsqrt(x);
+  r = qdfast::mul(x, inv);
+}
+#endif
 
 // Binary exponentiation, multiprec.hpp:431-441.  Starts from one and
 // multiplies result*base exactly like the reference (1*base is not elided:

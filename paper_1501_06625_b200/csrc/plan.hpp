@@ -69,6 +69,25 @@ inline int lane_k_batch(int L) {
   return L == 4 ? 4 : 128;
 }
 
+// Batch lane tasks are dealt to warps in bundles of 32 (one task per lane).
+// A bundle's contributions are stored as lane-interleaved streams: entry
+// (pos, lane) at pos*32 + lane holds that lane's contribution number
+// pos - s (workspace index + the coefficient itself), so a warp loading
+// contribution r of all its lanes issues one coalesced 128-byte index load
+// and 2L coalesced coefficient loads.  Tasks are ordered column-major before
+// bundling: for systems whose equations share a support (the random dense
+// batch system) the 32 lanes of a bundle then read the SAME workspace entry
+// at every step (a broadcast) -- no gathers anywhere.  Summation order is
+// unchanged (each lane runs the canonical width-32 tree of its own slot).
+struct Bundle {
+  int32_t task_beg, ntasks;  // lane l < ntasks runs btasks[task_beg + l]
+  int32_t sg, kg;            // g stream: rows sg .. sg+kg-1 (kg = max g_cnt over the lanes)
+  int32_t sf, kf;            // f stream (kf = 0 when every lane is shared)
+  int32_t pad0, pad1;
+};
+constexpr int kBundleWarps = 8;            // warps of a batch CTA (device.cuh kWarps)
+constexpr int64_t kStreamCap = 64L << 20;  // stream entries (x 32 lanes x (4 + 16L) bytes) before giving up
+
 struct HostPlan {
   int n = 0, N = 0, L = 1;
   // monomials (device order)
@@ -80,6 +99,13 @@ struct HostPlan {
   std::vector<SlotTask> tasks_b;                // batch partition (lane_k_batch)
   int32_t class_beg_b[6] = {0, 0, 0, 0, 0, 0};
   std::vector<int32_t> ctr_coef, ctr_ws;
+  // batch lane-task bundles (empty: the batch runs its lane tasks unbundled)
+  std::vector<Bundle> bundles;            // ordered by warp: warp w runs [bundle_warp_beg[w], [w+1])
+  int32_t bundle_warp_beg[kBundleWarps + 1] = {};
+  std::vector<SlotTask> btasks;           // lane tasks in bundle order
+  std::vector<int32_t> s_ws;              // [s_len][32] workspace index (-1: constant term)
+  std::vector<double> s_coef;             // [2L][s_len * 32] coefficient limbs
+  int64_t s_len = 0;
   // coefficients of all terms of g then f, complex SoA [2][L][n_coef]
   std::vector<double> coef;
   int64_t n_coef = 0;
@@ -104,6 +130,72 @@ inline void validate(const pt_system_desc* s) {
       if (q > s->term_ptr[t]) check(s->var[q] > s->var[q - 1], "support variables not strictly increasing");
     }
   }
+}
+
+// Bundles of the batch partition's lane tasks (class 0 of tasks_b), see Bundle.
+inline void build_bundles(HostPlan& P) {
+  const char* e = std::getenv("PT_BUNDLES");  // tuning knob: 0 disables the streams
+  if (e && e[0] == '0') return;
+  const int L = P.L;
+  std::vector<SlotTask> lt(P.tasks_b.begin() + P.class_beg_b[0], P.tasks_b.begin() + P.class_beg_b[1]);
+  if (lt.empty()) return;
+  std::stable_sort(lt.begin(), lt.end(), [](const SlotTask& a, const SlotTask& b) {
+    return a.col != b.col ? a.col < b.col : a.row < b.row;
+  });
+  int64_t len = 0;
+  std::vector<Bundle> bs;
+  for (size_t b0 = 0; b0 < lt.size(); b0 += 32) {
+    Bundle B{};
+    B.task_beg = (int32_t)b0;
+    B.ntasks = (int32_t)std::min<size_t>(32, lt.size() - b0);
+    for (int l = 0; l < B.ntasks; ++l) {
+      const SlotTask& t = lt[b0 + l];
+      B.kg = std::max(B.kg, t.g_cnt);
+      B.kf = std::max(B.kf, t.f_cnt);
+    }
+    B.sg = (int32_t)len;
+    len += B.kg;
+    B.sf = (int32_t)len;
+    len += B.kf;
+    bs.push_back(B);
+  }
+  if (len > kStreamCap) return;
+  P.s_len = std::max<int64_t>(len, 1);
+  const int64_t S = P.s_len * 32;
+  P.s_ws.assign((size_t)S, 0);
+  P.s_coef.assign((size_t)2 * L * S, 0.0);
+  auto fill = [&](int64_t row, int lane, int32_t beg, int32_t cnt) {
+    for (int32_t r = 0; r < cnt; ++r) {
+      const int64_t at = (row + r) * 32 + lane;
+      const int32_t ci = P.ctr_coef[beg + r];
+      P.s_ws[at] = P.ctr_ws[beg + r];
+      for (int q = 0; q < 2 * L; ++q) P.s_coef[(size_t)q * S + at] = P.coef[(size_t)q * P.n_coef + ci];
+    }
+  };
+  for (const Bundle& B : bs)
+    for (int l = 0; l < B.ntasks; ++l) {
+      const SlotTask& t = lt[B.task_beg + l];
+      fill(B.sg, l, t.g_beg, t.g_cnt);
+      if (t.f_cnt > 0) fill(B.sf, l, t.f_beg, t.f_cnt);
+    }
+  // deal bundles to the warps, largest first onto the least loaded warp
+  std::vector<int> ord(bs.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return bs[a].kg + bs[a].kf > bs[b].kg + bs[b].kf; });
+  std::vector<std::vector<int>> per(kBundleWarps);
+  std::vector<int64_t> load(kBundleWarps, 0);
+  for (int b : ord) {
+    const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    per[w].push_back(b);
+    load[w] += bs[b].kg + bs[b].kf + 8;
+  }
+  P.bundles.clear();
+  for (int w = 0; w < kBundleWarps; ++w) {
+    P.bundle_warp_beg[w] = (int32_t)P.bundles.size();
+    for (int b : per[w]) P.bundles.push_back(bs[b]);
+  }
+  P.bundle_warp_beg[kBundleWarps] = (int32_t)P.bundles.size();
+  P.btasks = std::move(lt);
 }
 
 inline HostPlan compile(const pt_system_desc* g, const pt_system_desc* f, int L) {
@@ -290,6 +382,7 @@ inline HostPlan compile(const pt_system_desc* g, const pt_system_desc* f, int L)
   };
   partition(lane_k(L), P.tasks, P.class_beg);
   partition(lane_k_batch(L), P.tasks_b, P.class_beg_b);
+  build_bundles(P);
   if (P.ctr_coef.empty()) {
     P.ctr_coef.push_back(0);
     P.ctr_ws.push_back(-1);

@@ -39,6 +39,7 @@ inline const KernelSet& kset(pt_prec p) { return p == PT_D ? kset_d : (p == PT_D
 // kernels that follow the reference's non-finite rules exactly: the DD set
 // differs (kset_dd skips dd_norm's non-finite select); D and QD are exact as is
 inline const KernelSet& kset_exact(pt_prec p) { return p == PT_DD ? kset_dd_exact : kset(p); }
+inline const KernelSet& kset_mode(pt_prec p, int arith) { return (p == PT_QD && arith == 1) ? kset_qd_fast : kset_exact(p); }
 
 // Launch a kernel (as a cluster of `cluster` CTAs when cluster > 0) from its
 // untyped pointer.
@@ -80,10 +81,19 @@ struct pt_plan {
   int grid_warp = 0, cluster_warp = 0, batch_warp = 0;  // warp-per-column MGS per engine
   const ptplan::SlotTask* tasks_b = nullptr;            // batch partition of the slot tasks
   int class_beg_b[6] = {0, 0, 0, 0, 0, 0};
+  // batch bundles over lane-interleaved contribution streams (plan.hpp Bundle)
+  const ptplan::Bundle* bundles = nullptr;
+  int bundle_warp_beg[kWarps + 1] = {};
+  const ptplan::SlotTask* btasks = nullptr;
+  const int32_t* s_ws = nullptr;
+  const double* s_coef = nullptr;
+  long s_len = 0;
+  int arith = 0;              // PT_ARITH_REFERENCE / PT_ARITH_FAST (QD only)
   int engine = 0;             // 0 grid, 1 cluster (single path)
   int cluster_size = 0;       // CTAs of the cluster engine (0: unavailable)
   size_t cluster_dyn_smem = 0;
   size_t batch_dyn_smem = 0;  // dynamic smem of k_track_batch
+  int batch_mgs = 0;          // k_track_batch runs mgs_batch (N <= kBmMaxN)
   // staging for the host-buffer API
   double* d_start = nullptr;
   double* d_end = nullptr;
@@ -106,6 +116,11 @@ struct pt_plan {
 
 namespace {
 
+
+// the plan's tracking kernels, and those that follow the reference's
+// non-finite rules (the DD re-track set; the same set otherwise)
+inline const KernelSet& tset(const pt_plan* p) { return p->arith ? kset_qd_fast : kset(p->prec); }
+inline const KernelSet& tset_exact(const pt_plan* p) { return p->arith ? kset_qd_fast : kset_exact(p->prec); }
 
 int occupancy_blocks(const void* fn, int device, int* per_sm, int* sms) {
   cudaDeviceProp prop;
@@ -303,11 +318,11 @@ void launch_engine(pt_plan* p, const KernelSet& ks, const pt_step_params& sp, co
 // track_path on the device: the fast kernels, then (DD) the exact re-track
 // launch, which exits at once unless the fast run flagged PT_STAT_NONFINITE.
 void launch_grid(pt_plan* p, const pt_step_params& sp, const TrackIO& io, cudaStream_t s, cudaError_t* err) {
-  launch_engine(p, kset(p->prec), sp, io, s, err);
-  if (*err != cudaSuccess || &kset_exact(p->prec) == &kset(p->prec)) return;
+  launch_engine(p, tset(p), sp, io, s, err);
+  if (*err != cudaSuccess || &tset_exact(p) == &tset(p)) return;
   TrackIO re = io;
   re.retrack = 1;
-  launch_engine(p, kset_exact(p->prec), sp, re, s, err);
+  launch_engine(p, tset_exact(p), sp, re, s, err);
 }
 
 int validate_params(const pt_step_params* sp) {
@@ -390,7 +405,11 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
         {hp.tasks.data(), hp.tasks.size() * sizeof(ptplan::SlotTask)},
         {hp.ctr_coef.data(), hp.ctr_coef.size() * 4},   {hp.ctr_ws.data(), hp.ctr_ws.size() * 4},
         {hp.coef.data(), hp.coef.size() * 8},           {gamma, (size_t)2 * L * 8},
-        {hp.tasks_b.data(), hp.tasks_b.size() * sizeof(ptplan::SlotTask)}};
+        {hp.tasks_b.data(), hp.tasks_b.size() * sizeof(ptplan::SlotTask)},
+        {hp.bundles.data(), hp.bundles.size() * sizeof(ptplan::Bundle)},
+        {hp.btasks.data(), hp.btasks.size() * sizeof(ptplan::SlotTask)},
+        {hp.s_ws.data(), hp.s_ws.size() * 4},
+        {hp.s_coef.data(), hp.s_coef.size() * 8}};
     size_t total = 0;
     std::vector<size_t> offs;
     for (auto& pc : pieces) {
@@ -424,6 +443,15 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     for (int c = 0; c < 6; ++c) dp.class_beg[c] = hp.class_beg[c];
     p->tasks_b = (const ptplan::SlotTask*)(base + offs[11]);
     for (int c = 0; c < 6; ++c) p->class_beg_b[c] = hp.class_beg_b[c];
+    if (!hp.bundles.empty()) {
+      static_assert(ptplan::kBundleWarps == kWarps, "bundles are dealt to the warps of a batch CTA");
+      p->bundles = (const ptplan::Bundle*)(base + offs[12]);
+      for (int w = 0; w <= kWarps; ++w) p->bundle_warp_beg[w] = hp.bundle_warp_beg[w];
+      p->btasks = (const ptplan::SlotTask*)(base + offs[13]);
+      p->s_ws = (const int32_t*)(base + offs[14]);
+      p->s_coef = (const double*)(base + offs[15]);
+      p->s_len = (long)hp.s_len;
+    }
     dp.ctr_coef = (const int32_t*)(base + offs[7]);
     dp.ctr_ws = (const int32_t*)(base + offs[8]);
     dp.coef = (const double*)(base + offs[9]);
@@ -489,6 +517,15 @@ int pt_plan_set_engine(pt_plan* p, int32_t engine) {
   if (!p || engine < 0 || engine > 1) return fail(PT_E_INVAL, "engine must be 0 (grid) or 1 (cluster)");
   if (engine == 1 && p->cluster_size == 0) return fail(PT_E_INVAL, "no schedulable cluster for this plan");
   p->engine = engine;
+  return PT_OK;
+}
+
+int pt_plan_set_arith(pt_plan* p, int32_t arith) {
+  if (!p || (arith != PT_ARITH_REFERENCE && arith != PT_ARITH_FAST)) return fail(PT_E_INVAL, "bad arithmetic");
+  if (arith == PT_ARITH_FAST && p->prec != PT_QD) return fail(PT_E_INVAL, "PT_ARITH_FAST exists for QD plans only");
+  if (arith == PT_ARITH_FAST)  // the fast set is launched with the reference set's geometry
+    PT_CUDA(cudaFuncSetAttribute(kset_qd_fast.track_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  p->arith = arith;
   return PT_OK;
 }
 
@@ -675,6 +712,13 @@ static int ensure_batch(pt_plan* p) {
   int per_sm = 0, sms = 0;
   const void* fn = kset(p->prec).track_batch;
   p->batch_dyn_smem = engine_smem(p->L, p->N, p->n, 1, true, &p->batch_warp);
+  const char* be = getenv("PT_MGS_BATCH");  // tuning knob: 0 keeps the warp / group MGS in the batch
+  p->batch_mgs = (p->N <= kBmMaxN && !(be && be[0] == '0')) ? 1 : 0;
+  if (p->batch_mgs) {  // the padded matrix, then (after the MGS) the staged R and the x copy reuse it
+    p->batch_warp = 0;
+    p->batch_dyn_smem = std::max({bm_smem_doubles(p->L, p->N, p->n), backsub_stage_doubles(p->L, p->n),
+                                  (size_t)2 * p->L * p->n}) * 8;
+  }
   int rc = set_dyn_smem(fn, p->batch_dyn_smem);
   if (rc) return rc;
   cudaDeviceProp prop;
@@ -704,17 +748,24 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
   PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 16, s));
-  rc = set_dyn_smem(kset(p->prec).track_batch, p->batch_dyn_smem);  // per-function attribute: this plan's value
+  rc = set_dyn_smem(tset(p).track_batch, p->batch_dyn_smem);  // per-function attribute: this plan's value
   if (rc) return rc;
   const unsigned long long epoch = (++p->launches) << 40;
   const int blocks = std::min(p->batch_blocks, n_paths);
   DevPlan bdp = p->dp;
   bdp.mgs_smem = p->batch_dyn_smem > 0;
   bdp.mgs_warp = p->batch_warp;
+  bdp.mgs_batch = p->batch_mgs;
   bdp.bs_smem = stage_fits(p, p->batch_dyn_smem);
   bdp.x_smem = x_fits(p, p->batch_dyn_smem);
   bdp.tasks = p->tasks_b;
   for (int c = 0; c < 6; ++c) bdp.class_beg[c] = p->class_beg_b[c];
+  bdp.bundles = p->bundles;
+  for (int w = 0; w <= kWarps; ++w) bdp.bundle_warp_beg[w] = p->bundle_warp_beg[w];
+  bdp.btasks = p->btasks;
+  bdp.s_ws = p->s_ws;
+  bdp.s_coef = p->s_coef;
+  bdp.s_len = p->s_len;
   // launched as clusters of one CTA: the warp MGS pushes q_k with st.async,
   // which needs a cluster launch even when the cluster is the CTA itself
   Layout lay = p->lay;
@@ -723,16 +774,16 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   unsigned long long ep = epoch;
   int retrack = 0;
   void* args[] = {&bdp, &p->bwork, &p->bu, &lay, &spc, &d_starts, &d_ends, &d_stats, &np, &p->d_queue, &ep, &retrack};
-  PT_CUDA(launch_ex(kset(p->prec).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
-  if (&kset_exact(p->prec) != &kset(p->prec)) {
+  PT_CUDA(launch_ex(tset(p).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
+  if (&tset_exact(p) != &tset(p)) {
     // exact re-track of the paths whose fast run met a non-finite value
     // (PT_STAT_NONFINITE): the queue restarts, the abort word is kept
     PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 8, s));
-    rc = set_dyn_smem(kset_exact(p->prec).track_batch, p->batch_dyn_smem);
+    rc = set_dyn_smem(tset_exact(p).track_batch, p->batch_dyn_smem);
     if (rc) return rc;
     retrack = 1;
     ep = (++p->launches) << 40;
-    PT_CUDA(launch_ex(kset_exact(p->prec).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
+    PT_CUDA(launch_ex(tset_exact(p).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
   }
   PT_CUDA(cudaGetLastError());
   return PT_OK;
@@ -786,7 +837,7 @@ int pt_eval_homotopy(pt_plan* p, const double* x, double t, double* h, double* J
   dp.mgs_smem = 0;
   dp.mgs_warp = 0;
   void* args[] = {&dp, &W, &dx, &t, &dh, &dJ, &dr};
-  const void* fn = kset_exact(p->prec).eval;
+  const void* fn = tset_exact(p).eval;
   rc = set_dyn_smem(fn, p->grid_dyn_smem);
   if (rc) return rc;
   PT_CUDA(cudaMemset(W.ctl, 0, CTL_WORDS * sizeof(unsigned long long)));
@@ -817,7 +868,7 @@ int pt_eval_bench(pt_plan* p, const double* x, double t, int32_t reps, double* m
   dp.mgs_warp = 0;
   double* null = nullptr;
   void* args[] = {&dp, &W, &dx, &t, &null, &null, &null};
-  const void* fn = kset_exact(p->prec).eval;
+  const void* fn = tset_exact(p).eval;
   rc = set_dyn_smem(fn, p->grid_dyn_smem);
   if (rc) return rc;
   PT_CUDA(cudaMemset(W.ctl, 0, CTL_WORDS * sizeof(unsigned long long)));
@@ -915,6 +966,13 @@ int pt_arith_host(pt_prec prec, int32_t op, int64_t count, const double* a, cons
 
 int pt_arith_device(int device, pt_prec prec, int32_t op, int64_t count, const double* a, const double* b,
                     double* out) {
+  return pt_arith_device_mode(device, prec, PT_ARITH_REFERENCE, op, count, a, b, out);
+}
+
+int pt_arith_device_mode(int device, pt_prec prec, int32_t arith, int32_t op, int64_t count, const double* a,
+                         const double* b, double* out) {
+  if (arith != PT_ARITH_REFERENCE && !(arith == PT_ARITH_FAST && prec == PT_QD))
+    return fail(PT_E_INVAL, "PT_ARITH_FAST exists for QD only");
   if (!a || !b || !out || count < 0) return fail(PT_E_INVAL, "bad arith args");
   int rc = check_device(device);
   if (rc) return rc;
@@ -930,7 +988,7 @@ int pt_arith_device(int device, pt_prec prec, int32_t op, int64_t count, const d
   long cnt = (long)count;
   int opc = op;
   void* args[] = {&opc, &cnt, &da, &db, &dout};
-  PT_CUDA(cudaLaunchKernel(kset_exact(prec).arith, dim3(blocks), dim3(256), args, 0, 0));
+  PT_CUDA(cudaLaunchKernel(kset_mode(prec, arith).arith, dim3(blocks), dim3(256), args, 0, 0));
   PT_CUDA(cudaGetLastError());
   PT_CUDA(cudaDeviceSynchronize());
   PT_CUDA(cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost));

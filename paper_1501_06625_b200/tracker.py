@@ -119,6 +119,12 @@ class Homotopy:
         """Force the single-path engine ("grid" or "cluster"); results are bit-identical."""
         nat.check(nat.lib.pt_plan_set_engine(self._plan, {"grid": 0, "cluster": 1}[engine]))
 
+    def set_arith(self, arith: str) -> None:
+        """"reference" (default: the reference's operation sequences, bit
+        parity) or "fast" (QD plans: tolerance-parity quad-double arithmetic,
+        pt_plan_set_arith)."""
+        nat.check(nat.lib.pt_plan_set_arith(self._plan, {"reference": 0, "fast": 1}[arith]))
+
     def track_path(self, start: np.ndarray, params: Optional[StepControlParams] = None,
                    trace: bool = False) -> TrackOutcome:
         """track_path (SPEC.md:466-474)."""
@@ -190,15 +196,19 @@ def device_count() -> int:
     return int(nat.lib.pt_device_count())
 
 
-def arith(prec: PrecisionMode, op: int, a: np.ndarray, b: np.ndarray, device: Optional[int] = 0) -> np.ndarray:
+def arith(prec: PrecisionMode, op: int, a: np.ndarray, b: np.ndarray, device: Optional[int] = 0,
+          fast: bool = False) -> np.ndarray:
     """Bulk scalar op (parity tests). device=None runs the host build of the
-    device arithmetic."""
+    device arithmetic; fast=True the tolerance-parity QD set on the device."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     out = np.zeros_like(a)
     cnt = a.size // (2 * prec.limbs)
     if device is None:
         nat.check(nat.lib.pt_arith_host(int(prec), op, cnt, nat.dptr(a), nat.dptr(b), nat.dptr(out)))
+    elif fast:
+        nat.check(nat.lib.pt_arith_device_mode(device, int(prec), 1, op, cnt, nat.dptr(a), nat.dptr(b),
+                                               nat.dptr(out)))
     else:
         nat.check(nat.lib.pt_arith_device(device, int(prec), op, cnt, nat.dptr(a), nat.dptr(b), nat.dptr(out)))
     return out

@@ -1,4 +1,4 @@
-"""Phase timers of batch CTA 0 (k_track_batch): python tools/prof_batch.py [prec] [paths]"""
+"""Phase timers of batch CTA 0 (k_track_batch): python tools/prof_batch.py [prec] [paths] [max_steps]"""
 import json
 import os
 import sys
@@ -13,6 +13,8 @@ from paper_1501_06625_b200 import _native as nat, workloads as W  # noqa: E402
 prec = pt.PrecisionMode.parse(sys.argv[1] if len(sys.argv) > 1 else "dd")
 npaths = int(sys.argv[2]) if len(sys.argv) > 2 else 296
 w = W.batch(prec=prec)
+if len(sys.argv) > 3:
+    w.params.max_steps = int(sys.argv[3])
 hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k)
 starts = np.ascontiguousarray(w.starts[:npaths])
 hom.track_batch(starts[:8], w.params)  # allocate the batch workspace
