@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--cpu-paths", type=int, default=96, help="batch: CPU sample paths per reference step")
     ap.add_argument("--no-cpu-reference", action="store_true",
                     help="skip the precision-matched CPU tracker timing (keep the CPU-D comparison)")
+    ap.add_argument("--arith", default="reference", choices=["reference", "fast"],
+                    help="QD only: fast = tolerance-parity quad-double arithmetic (pt_plan_set_arith)")
     ap.add_argument("--max-steps", type=int, default=None,
                     help="track only a prefix of the path (per-step timing of huge configs)")
     return ap.parse_args()
@@ -96,6 +98,8 @@ def apply_overrides(args, w):
     if args.max_steps is not None:
         w.params.max_steps = args.max_steps
         w.name += f"-prefix{args.max_steps}"
+    if args.arith == "fast":
+        w.name += "-fastqd"
     return w
 
 
@@ -107,6 +111,7 @@ def metric_of(args, w):
 
 def config(args, w, world):
     cfg = {"workload": w.name, "n_vars": w.n, "n_eqs": w.N, "precision": w.prec.name.lower(),
+           "arith": "reference (bit parity)" if args.arith == "reference" else "fast (tolerance parity)",
            "l2": "flushed between steps (256 MiB write)"}
     if is_batch(args):
         cfg.update({"batch_paths": int(w.starts.shape[0]), "paths_per_step_per_gpu": args.paths_per_step,
@@ -330,6 +335,8 @@ def run_ours(args):
     w = apply_overrides(args, workload(args))
     batch = is_batch(args)
     hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=device)
+    if args.arith == "fast":
+        hom.set_arith("fast")  # tolerance parity (tests/test_qdfast.py), QD plans only
     sp = w.params.native()
     stream = torch.cuda.Stream(device)  # kernel and its CUDA events on the same stream
     sh = C.c_void_p(stream.cuda_stream)

@@ -31,7 +31,11 @@ namespace ptdev {
 
 using namespace ptk;
 
-constexpr int kThreads = 256;  // every tracker CTA
+// every tracker CTA.  (Measured on the batch: 4 x 128-thread CTAs per SM
+// instead of 2 x 256 cut the barrier stalls but almost doubled the
+// instruction-cache stalls -- 4 CTAs in 4 different phases -- and ran 27 %
+// slower.)
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxRowsPerThread = 2;  // n <= 512
 constexpr int kMaxDegree = 8;
@@ -62,6 +66,7 @@ struct DevPlan {
   const double* gamma;  // 2L limbs
   int relax_k;
   int mgs_smem;  // 1: MGS keeps owned columns in dynamic shared memory
+  int dyn_smem;  // 1: the launch has dynamic shared memory (x copy, split scratch, staged R)
   int mgs_warp;  // 1: warp-per-column MGS + one-warp back substitution (mgs_warp.cuh, N <= 128)
   int mgs_B;     // warp MGS: consecutive columns per CTA block (divides kWarps)
   int bs_smem;   // warp back substitution stages R in CTA 0's dynamic shared memory
@@ -70,7 +75,10 @@ struct DevPlan {
   // batch only (BlockTeam): lane tasks as warp bundles over lane-interleaved
   // contribution streams (plan.hpp Bundle); bundles == nullptr: unbundled
   const ptplan::Bundle* bundles;
-  int bundle_warp_beg[kWarps + 1];
+  int n_bundles;
+  const int32_t* splits;  // split groups: (task_beg, ntasks, D, scratch base) x n_splits
+  int n_splits;
+  int scratch_units;      // 32-lane complex rows of split scratch (dynamic smem after the x copy)
   const ptplan::SlotTask* btasks;
   const int32_t* s_ws;
   const double* s_coef;
@@ -464,6 +472,7 @@ struct Smem {
   double pmax[kMaxCols];    // MGS prefix max of r_kk (cluster / block teams)
   int flag;
   int mgs_seq;              // MGS sweeps completed by this CTA in this launch (mbarrier phase parity)
+  int bundle_next;          // batch: next bundle to claim (reset before every evaluation)
 };
 
 // ---------------------------------------------------------------------------
@@ -698,47 +707,87 @@ __device__ __forceinline__ cplx<R> lane_sum(const DevPlan& P, const Work& W, int
 // structure is warp-uniform (u), only the K tests are per lane.
 __host__ __device__ constexpr int brev3(int u) { return ((u & 1) << 2) | (u & 2) | ((u & 4) >> 2); }
 
+// General form: the subtree of the canonical width-P tree over the leaves
+// p = c + D t (t < W = P / D, 4 <= W <= 32) -- D = 1 is the whole tree; the
+// batch splits long sums over D lanes and merges the D subtrees with the
+// levels off = D/2 .. 1 afterwards (tree_combine).  The leaves t0 + mG
+// (G = W / 4, m = 0..3) form Q(t0) (levels off = W/2, W/4 of the subtree);
+// the Q's are merged in bit-reversed order t0 = brev(u) through a stack of up
+// to three levels, each merge skipped when its right subtree's least leaf
+// index is >= K.
+__device__ __forceinline__ int brev_g(int u, int G) {
+  return G == 8 ? brev3(u) : (G == 4 ? (((u & 1) << 1) | ((u & 2) >> 1)) : (G == 2 ? u : 0));
+}
+
 template <class R, class Get>
-__device__ __forceinline__ cplx<R> lane_canon32_g(int K, const Get& get) {
-  cplx<R> A = c_zero<R>(), B = c_zero<R>(), C = c_zero<R>();
+__device__ __forceinline__ cplx<R> lane_tree_g(int K, int P, int D, int c, const Get& get) {
+  cplx<R> A = c_zero<R>(), B = c_zero<R>(), C = c_zero<R>(), q = c_zero<R>();
+  if (c >= K) return q;  // the subtree is empty
+  const int G = P / (4 * D);
 #pragma unroll 1
-  for (int u = 0; u < 8; ++u) {
-    const int c = brev3(u);
-    cplx<R> q = c_zero<R>();
-    if (c < K) {  // Q(c) exists: leaves c + 8m, m = 0..3, summed round by round (c[p], c[p+32], ...)
+  for (int u = 0; u < G; ++u) {
+    const int t0 = brev_g(u, G);
+    const int p0 = c + D * t0;
+    q = c_zero<R>();
+    if (p0 < K) {  // Q(t0) exists: leaves p0 + m D G, summed round by round (c[p], c[p+P], ...)
+      const int dg = D * G;
       cplx<R> l[4] = {c_zero<R>(), c_zero<R>(), c_zero<R>(), c_zero<R>()};
 #pragma unroll 1
-      for (int r0 = 0; r0 < K; r0 += 32) {
+      for (int r0 = 0; p0 + r0 < K; r0 += P) {
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          const int p = c + 8 * m + r0;
-          if (p < K) {
-            const cplx<R> v = get(p);
+          const int r = p0 + m * dg + r0;
+          if (r < K) {
+            const cplx<R> v = get(r);
             l[m] = r0 == 0 ? v : c_add(l[m], v);
           }
         }
       }
       cplx<R> x = l[0], y = l[1];
-      if (c + 16 < K) x = c_add(x, l[2]);  // off = 16
-      if (c + 24 < K) y = c_add(y, l[3]);
-      q = c + 8 < K ? c_add(x, y) : x;     // off = 8
+      if (p0 + 2 * dg < K) x = c_add(x, l[2]);  // off = W/2 of the subtree
+      if (p0 + 3 * dg < K) y = c_add(y, l[3]);
+      q = p0 + dg < K ? c_add(x, y) : x;        // off = W/4
     }
+    if (G == 1) break;
     if ((u & 1) == 0) {
       A = q;
     } else {
-      if (c < K) A = c_add(A, q);  // level 4: right subtree {c}
-      if ((u & 2) == 0) {
-        B = A;
-      } else {
-        if (brev3(u - 1) < K) B = c_add(B, A);  // level 2
-        if ((u & 4) == 0)
-          C = B;
-        else if (brev3(u - 3) < K)
-          C = c_add(C, B);  // level 1
+      if (c + D * t0 < K) A = c_add(A, q);  // right subtree {u}
+      if (G >= 4) {
+        if ((u & 2) == 0) {
+          B = A;
+        } else {
+          if (c + D * brev_g(u - 1, G) < K) B = c_add(B, A);
+          if (G == 8) {
+            if ((u & 4) == 0)
+              C = B;
+            else if (c + D * brev_g(u - 3, G) < K)
+              C = c_add(C, B);
+          }
+        }
       }
     }
   }
-  return C;
+  return G == 1 ? q : (G == 2 ? A : (G == 4 ? B : C));
+}
+
+// Merge the D subtree sums v[c] (c < D) with the levels off = D/2 .. 1.
+template <class R>
+__device__ __forceinline__ cplx<R> tree_combine(cplx<R> (&v)[8], int D, int K) {
+#pragma unroll
+  for (int off = 4; off >= 1; off >>= 1) {
+    if (off < D) {
+#pragma unroll
+      for (int c = 0; c < off; ++c)
+        if (c + off < K) v[c] = c_add(v[c], v[c + off]);
+    }
+  }
+  return v[0];
+}
+
+template <class R, class Get>
+__device__ __forceinline__ cplx<R> lane_canon32_g(int K, const Get& get) {
+  return lane_tree_g<R>(K, 32, 1, 0, get);
 }
 
 template <class R>
@@ -760,8 +809,10 @@ __device__ __forceinline__ cplx<R> s_contrib(const DevPlan& P, const Work& W, lo
 
 // lane_canon32 over a stream (contribution r of this lane at (s0 + r)*32 + lane).
 template <class R>
-__device__ __forceinline__ cplx<R> lane_canon32_s(const DevPlan& P, const Work& W, long s0, int lane, int K) {
-  return lane_canon32_g<R>(K, [&](int r) { return s_contrib<R>(P, W, (s0 + r) * 32 + lane); });
+__device__ __forceinline__ cplx<R> lane_tree_s(const DevPlan& P, const Work& W, long s0, int lane, int K, int D,
+                                               int c) {
+  return lane_tree_g<R>(K, K > 0 ? width_eval_d(K) : 32, D, c,
+                        [&](int r) { return s_contrib<R>(P, W, (s0 + r) * 32 + lane); });
 }
 
 
@@ -786,44 +837,90 @@ __device__ __forceinline__ void slot_store(const DevPlan& P, const Work& W, cons
 
 // The batch's lane tasks: warp w runs its bundles (plan.hpp Bundle), lane l
 // the l-th slot of each.  Own register-allocation unit (the unrolled trees).
+// The batch's lane tasks: warps claim bundles (plan.hpp Bundle) from a
+// shared counter, largest first; lane l runs the l-th slot of a bundle.  A
+// split bundle (D > 1) computes only the subtree c of its slots' sums and
+// parks it in shared scratch; after one CTA barrier the D subtrees of each
+// split group are merged (tree_combine) and stored.  Own register-allocation
+// unit; one copy of the tree for g and f (instruction cache).
 template <class R>
-__device__ __noinline__ void eval_bundles(const DevPlan& P, const Work& W, const cplx<R> wS, const R wT) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int b = P.bundle_warp_beg[warp]; b < P.bundle_warp_beg[warp + 1]; ++b) {
+__device__ __noinline__ void eval_bundles(const DevPlan& P, const Work& W, const cplx<R> wS, const R wT, int* next,
+                                          double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int L = limbs_of<R>::L;
+  const long SS = (long)P.scratch_units * 32;  // complex entries of the scratch (plane stride)
+  for (;;) {
+    int b = 0;
+    if (lane == 0) b = atomicAdd(next, 1);  // largest bundles first: greedy list scheduling over the warps
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (b >= P.n_bundles) break;
     const ptplan::Bundle B = P.bundles[b];
+    const int D = B.dc >> 8, c = B.dc & 255;
     if (lane < B.ntasks) {
       const ptplan::SlotTask tk = P.btasks[B.task_beg + lane];
       cplx<R> Sg = c_zero<R>(), Sf = c_zero<R>();
 #pragma unroll 1
-      for (int side = 0; side < 2; ++side) {  // one copy of the tree for g and f (instruction cache)
+      for (int side = 0; side < 2; ++side) {
         const int K = side ? tk.f_cnt : tk.g_cnt;
-        const cplx<R> v = lane_canon32_s<R>(P, W, side ? B.sf : B.sg, lane, K);
+        const cplx<R> v = lane_tree_s<R>(P, W, side ? B.sf : B.sg, lane, K, D, c);
         if (side)
           Sf = v;
         else
           Sg = v;
       }
-      bool have_f;
-      if (tk.f_cnt < 0) {
-        Sf = Sg;
-        have_f = tk.g_cnt > 0;
+      if (D == 1) {
+        bool have_f;
+        if (tk.f_cnt < 0) {
+          Sf = Sg;
+          have_f = tk.g_cnt > 0;
+        } else {
+          have_f = tk.f_cnt > 0;
+        }
+        slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);
       } else {
-        have_f = tk.f_cnt > 0;
+        store_c<R>(scratch, SS, (long)(B.split + c) * 32 + lane, Sg);
+        store_c<R>(scratch, SS, (long)(B.split + D + c) * 32 + lane, Sf);
       }
-      slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);
     }
   }
+  if (P.n_splits == 0) return;
+  __syncthreads();  // every split subtree parked
+  for (int gi = warp; gi < P.n_splits; gi += kWarps) {
+    const int32_t* sp = P.splits + 4 * gi;  // task_beg, ntasks, D, scratch base
+    if (lane >= sp[1]) continue;
+    const ptplan::SlotTask tk = P.btasks[sp[0] + lane];
+    const int D = sp[2], base = sp[3];
+    cplx<R> v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = c < D ? load_c<R>(scratch, SS, (long)(base + c) * 32 + lane) : c_zero<R>();
+    const cplx<R> Sg = tree_combine<R>(v, D, tk.g_cnt);
+    cplx<R> Sf;
+    bool have_f;
+    if (tk.f_cnt < 0) {
+      Sf = Sg;
+      have_f = tk.g_cnt > 0;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        v[c] = c < D ? load_c<R>(scratch, SS, (long)(base + D + c) * 32 + lane) : c_zero<R>();
+      Sf = tree_combine<R>(v, D, tk.f_cnt);
+      have_f = tk.f_cnt > 0;
+    }
+    slot_store<R>(P, W, tk, Sg, Sf, have_f, wS, wT);
+  }
+  (void)L;
 }
 
 template <class R, class Team>
-__device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double t) {
+__device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const Team& team, Smem<R>& sh, double t,
+                                       double* scratch = nullptr) {
   __syncwarp();  // whole warps call this: converged entry (no WARPSYNC.COLLECTIVE fallback for its shuffles)
   cplx<R> wS;
   R wT;
   weights<R>(P, t, wS, wT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (P.bundles != nullptr) {  // batch: lane tasks in warp bundles over coalesced streams
-    eval_bundles<R>(P, W, wS, wT);
+    eval_bundles<R>(P, W, wS, wT, &sh.bundle_next, scratch);
   } else {  // lane tasks: one slot per lane (canonical width 32, K <= lane_k)
     constexpr int KM = limbs_of<R>::L == 4 ? 4 : 8;
     const int beg = P.class_beg[0], end = P.class_beg[1];
@@ -847,6 +944,7 @@ __device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const T
 #pragma unroll 1
   for (int c = 0; c < 4; ++c) {  // rolled: one copy of the group sums (instruction cache)
     const int gw = 8 >> c;
+    if (gw > kWarps) continue;  // 128-thread batch CTAs: the host never leaves 8-warp tasks for them
     const int gpc = kWarps / gw;
     const int gi = warp / gw;
     Group g{gw, (warp % gw) * 32 + lane, 1 + gi};
@@ -1417,10 +1515,12 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
       __syncthreads();
       xs = colsm;
     }
+    if (threadIdx.x == 0) sh.bundle_next = 0;  // published by the team barrier below
     eval_monomials<R>(P, W, xs, tid, nth);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_MONO);
-    eval_slots<R, Team>(P, W, team, sh, t);
+    // split-bundle scratch: the batch's dynamic smem after the x copy
+    eval_slots<R, Team>(P, W, team, sh, t, colsm ? colsm + ((2L * limbs_of<R>::L * P.n + 31) & ~31L) : nullptr);
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_SLOTS);
     double r = 0.0;
@@ -1444,7 +1544,7 @@ __device__ NewtonOut newton(const DevPlan& P, const Work& W, const Team& team, S
     } else if (P.mgs_warp) {
       mgs_warp<R, Team>(P, W, team, sh, colsm, epoch, sqrt_eps);
     } else {
-      mgs<R, Team>(P, W, team, sh, colsm, Team::kQInGlobal ? nullptr : sh.pmax, epoch, sqrt_eps);
+      mgs<R, Team>(P, W, team, sh, P.mgs_smem ? colsm : nullptr, Team::kQInGlobal ? nullptr : sh.pmax, epoch, sqrt_eps);
     }
     if (!team.sync(&sh.flag)) return {0, NW_ABORT, it, -1.0, -1.0, 0, 0};
     pc.lap(W.prof + PROF_MGS);

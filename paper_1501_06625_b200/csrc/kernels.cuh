@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};
   cta_prologue<R>(P, sh, dyn_smem, (int)gridDim.x);
   __syncthreads();
-  track_path<R, GridTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
+  track_path<R, GridTeam>(P, W, team, sh, P.dyn_smem ? dyn_smem : nullptr, sp, io, epoch_base);
 }
 
 // One path on one thread-block cluster (launched with a cluster dimension
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const ClusterTeam team{W.ctl, (int)cluster_nranks(), (int)cluster_rank(), s_flags};
   cta_prologue<R>(P, sh, dyn_smem, team.nblocks);
   team.sync(&sh.flag);
-  track_path<R, ClusterTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io, epoch_base);
+  track_path<R, ClusterTeam>(P, W, team, sh, P.dyn_smem ? dyn_smem : nullptr, sp, io, epoch_base);
   team.sync(&sh.flag);  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, kBatchCtasPerSm<R>)
     // exact re-track launch: only the paths whose fast run met a non-finite value
     if (retrack && !(((volatile const pt_path_stats*)(stats + p))->flags & PT_STAT_NONFINITE)) continue;
     TrackIO io{starts + p * PS, ends + p * PS, stats + p, nullptr, 0, nullptr, 0};
-    track_path<R, BlockTeam>(P, W, team, sh, P.mgs_smem ? dyn_smem : nullptr, sp, io,
+    track_path<R, BlockTeam>(P, W, team, sh, P.dyn_smem ? dyn_smem : nullptr, sp, io,
                              epoch_base + ((unsigned long long)p << 16));
     // watchdog abort (the stats of path p say PT_FAIL_ABORT): this CTA's
     // exchange state is no longer trustworthy -- stop taking paths, tell the host

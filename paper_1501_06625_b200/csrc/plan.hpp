@@ -83,9 +83,9 @@ struct Bundle {
   int32_t task_beg, ntasks;  // lane l < ntasks runs btasks[task_beg + l]
   int32_t sg, kg;            // g stream: rows sg .. sg+kg-1 (kg = max g_cnt over the lanes)
   int32_t sf, kf;            // f stream (kf = 0 when every lane is shared)
-  int32_t pad0, pad1;
+  int32_t dc;                // D << 8 | c: the lanes sum the subtree c of D (D = 1: the whole slot)
+  int32_t split;             // D > 1: scratch row base of the split group (g: base + c, f: base + D + c)
 };
-constexpr int kBundleWarps = 8;            // warps of a batch CTA (device.cuh kWarps)
 constexpr int64_t kStreamCap = 64L << 20;  // stream entries (x 32 lanes x (4 + 16L) bytes) before giving up
 
 struct HostPlan {
@@ -100,8 +100,9 @@ struct HostPlan {
   int32_t class_beg_b[6] = {0, 0, 0, 0, 0, 0};
   std::vector<int32_t> ctr_coef, ctr_ws;
   // batch lane-task bundles (empty: the batch runs its lane tasks unbundled)
-  std::vector<Bundle> bundles;            // ordered by warp: warp w runs [bundle_warp_beg[w], [w+1])
-  int32_t bundle_warp_beg[kBundleWarps + 1] = {};
+  std::vector<Bundle> bundles;            // largest first (claimed by the warps through a shared counter)
+  std::vector<int32_t> splits;            // split groups: task_beg, ntasks, D, scratch row base
+  int32_t scratch_units = 0;              // 32-lane complex rows of split scratch
   std::vector<SlotTask> btasks;           // lane tasks in bundle order
   std::vector<int32_t> s_ws;              // [s_len][32] workspace index (-1: constant term)
   std::vector<double> s_coef;             // [2L][s_len * 32] coefficient limbs
@@ -132,32 +133,71 @@ inline void validate(const pt_system_desc* s) {
   }
 }
 
-// Bundles of the batch partition's lane tasks (class 0 of tasks_b), see Bundle.
+// Bundles of the batch partition (see Bundle): every slot whose canonical
+// widths are <= 128 on both sides becomes a lane task; a slot with many
+// contributions is split over D lanes (subtrees c = 0..D-1 of its tree,
+// D = pow2ceil(K / 128) within [P / 32, 8]) so no lane runs much more than
+// 128 contributions.  Tasks of one D are ordered column-major and dealt 32
+// per bundle; the remaining tasks stay in tasks_b's warp-group classes.
 inline void build_bundles(HostPlan& P) {
   const char* e = std::getenv("PT_BUNDLES");  // tuning knob: 0 disables the streams
   if (e && e[0] == '0') return;
   const int L = P.L;
-  std::vector<SlotTask> lt(P.tasks_b.begin() + P.class_beg_b[0], P.tasks_b.begin() + P.class_beg_b[1]);
-  if (lt.empty()) return;
-  std::stable_sort(lt.begin(), lt.end(), [](const SlotTask& a, const SlotTask& b) {
-    return a.col != b.col ? a.col < b.col : a.row < b.row;
-  });
-  int64_t len = 0;
-  std::vector<Bundle> bs;
-  for (size_t b0 = 0; b0 < lt.size(); b0 += 32) {
-    Bundle B{};
-    B.task_beg = (int32_t)b0;
-    B.ntasks = (int32_t)std::min<size_t>(32, lt.size() - b0);
-    for (int l = 0; l < B.ntasks; ++l) {
-      const SlotTask& t = lt[b0 + l];
-      B.kg = std::max(B.kg, t.g_cnt);
-      B.kf = std::max(B.kf, t.f_cnt);
+  auto width = [](int K) { return K > 0 ? width_eval(K) : 32; };
+  std::map<int, std::vector<SlotTask>> byD;
+  std::vector<SlotTask> rest;
+  for (const SlotTask& t : P.tasks_b) {
+    const int pmax = std::max(width(t.g_cnt), width(t.f_cnt));
+    if (pmax > 128) {
+      rest.push_back(t);
+      continue;
     }
-    B.sg = (int32_t)len;
-    len += B.kg;
-    B.sf = (int32_t)len;
-    len += B.kf;
-    bs.push_back(B);
+    const int kmax = std::max(t.g_cnt, t.f_cnt);
+    int D = pow2ceil((kmax + 127) / 128);
+    D = std::max(D, pmax / 32);
+    D = std::min(D, 8);
+    byD[D].push_back(t);
+  }
+  if (byD.empty()) return;
+  std::vector<SlotTask> lt;
+  std::vector<Bundle> bs;
+  std::vector<int32_t> splits;
+  int64_t len = 0;
+  int32_t units = 0;
+  for (auto& kv : byD) {
+    const int D = kv.first;
+    std::vector<SlotTask>& ts = kv.second;
+    std::stable_sort(ts.begin(), ts.end(), [](const SlotTask& a, const SlotTask& b) {
+      return a.col != b.col ? a.col < b.col : a.row < b.row;
+    });
+    for (size_t b0 = 0; b0 < ts.size(); b0 += 32) {
+      Bundle B{};
+      B.task_beg = (int32_t)lt.size();
+      B.ntasks = (int32_t)std::min<size_t>(32, ts.size() - b0);
+      for (int l = 0; l < B.ntasks; ++l) {
+        const SlotTask& t = ts[b0 + l];
+        lt.push_back(t);
+        B.kg = std::max(B.kg, t.g_cnt);
+        B.kf = std::max(B.kf, t.f_cnt);
+      }
+      B.sg = (int32_t)len;
+      len += B.kg;
+      B.sf = (int32_t)len;
+      len += B.kf;
+      B.split = -1;
+      if (D == 1) {
+        B.dc = 1 << 8;
+        bs.push_back(B);
+      } else {
+        splits.insert(splits.end(), {B.task_beg, B.ntasks, D, units});
+        B.split = units;
+        units += 2 * D;
+        for (int c = 0; c < D; ++c) {
+          B.dc = (D << 8) | c;
+          bs.push_back(B);
+        }
+      }
+    }
   }
   if (len > kStreamCap) return;
   P.s_len = std::max<int64_t>(len, 1);
@@ -172,30 +212,33 @@ inline void build_bundles(HostPlan& P) {
       for (int q = 0; q < 2 * L; ++q) P.s_coef[(size_t)q * S + at] = P.coef[(size_t)q * P.n_coef + ci];
     }
   };
-  for (const Bundle& B : bs)
+  for (const Bundle& B : bs) {
+    if ((B.dc & 255) != 0) continue;  // the sub-bundles of a split group share its streams
     for (int l = 0; l < B.ntasks; ++l) {
       const SlotTask& t = lt[B.task_beg + l];
       fill(B.sg, l, t.g_beg, t.g_cnt);
       if (t.f_cnt > 0) fill(B.sf, l, t.f_beg, t.f_cnt);
     }
-  // deal bundles to the warps, largest first onto the least loaded warp
-  std::vector<int> ord(bs.size());
-  for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
-  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return bs[a].kg + bs[a].kf > bs[b].kg + bs[b].kf; });
-  std::vector<std::vector<int>> per(kBundleWarps);
-  std::vector<int64_t> load(kBundleWarps, 0);
-  for (int b : ord) {
-    const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    per[w].push_back(b);
-    load[w] += bs[b].kg + bs[b].kf + 8;
   }
-  P.bundles.clear();
-  for (int w = 0; w < kBundleWarps; ++w) {
-    P.bundle_warp_beg[w] = (int32_t)P.bundles.size();
-    for (int b : per[w]) P.bundles.push_back(bs[b]);
-  }
-  P.bundle_warp_beg[kBundleWarps] = (int32_t)P.bundles.size();
+  // largest first: the warps of a batch CTA claim bundles in this order from a
+  // shared counter (greedy list scheduling, any warp count)
+  std::stable_sort(bs.begin(), bs.end(), [](const Bundle& x, const Bundle& y) {
+    return (x.kg + x.kf) / (x.dc >> 8) > (y.kg + y.kf) / (y.dc >> 8);
+  });
+  P.bundles = std::move(bs);
+  P.splits = std::move(splits);
+  P.scratch_units = units;
   P.btasks = std::move(lt);
+  // the batch's group classes keep only the slots that were not bundled
+  const int classes[5] = {0, 8, 4, 2, 1};
+  std::vector<SlotTask> out;
+  for (int c = 0; c < 5; ++c) {
+    P.class_beg_b[c] = (int32_t)out.size();
+    for (const auto& tk : rest)
+      if (tk.gw == classes[c]) out.push_back(tk);
+  }
+  P.class_beg_b[5] = (int32_t)out.size();
+  P.tasks_b = std::move(out);
 }
 
 inline HostPlan compile(const pt_system_desc* g, const pt_system_desc* f, int L) {

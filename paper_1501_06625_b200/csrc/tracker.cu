@@ -43,10 +43,11 @@ inline const KernelSet& kset_mode(pt_prec p, int arith) { return (p == PT_QD && 
 
 // Launch a kernel (as a cluster of `cluster` CTAs when cluster > 0) from its
 // untyped pointer.
-cudaError_t launch_ex(const void* fn, int grid, size_t smem, cudaStream_t s, int cluster, void** args) {
+cudaError_t launch_ex(const void* fn, int grid, size_t smem, cudaStream_t s, int cluster, void** args,
+                      int threads = kThreads) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -83,7 +84,9 @@ struct pt_plan {
   int class_beg_b[6] = {0, 0, 0, 0, 0, 0};
   // batch bundles over lane-interleaved contribution streams (plan.hpp Bundle)
   const ptplan::Bundle* bundles = nullptr;
-  int bundle_warp_beg[kWarps + 1] = {};
+  int n_bundles = 0;
+  const int32_t* splits = nullptr;
+  int n_splits = 0, scratch_units = 0;
   const ptplan::SlotTask* btasks = nullptr;
   const int32_t* s_ws = nullptr;
   const double* s_coef = nullptr;
@@ -94,6 +97,8 @@ struct pt_plan {
   size_t cluster_dyn_smem = 0;
   size_t batch_dyn_smem = 0;  // dynamic smem of k_track_batch
   int batch_mgs = 0;          // k_track_batch runs mgs_batch (N <= kBmMaxN)
+  int batch_mgs_smem = 0;     // the batch's MGS stages its columns in the dynamic smem
+  int batch_threads = kThreads;
   // staging for the host-buffer API
   double* d_start = nullptr;
   double* d_end = nullptr;
@@ -299,6 +304,7 @@ void launch_engine(pt_plan* p, const KernelSet& ks, const pt_step_params& sp, co
   if (p->engine == 1) {
     DevPlan dp = p->dp;
     dp.mgs_smem = p->cluster_dyn_smem > 0;
+    dp.dyn_smem = dp.mgs_smem;
     dp.mgs_warp = p->cluster_warp;
     dp.bs_smem = stage_fits(p, p->cluster_dyn_smem);
     dp.x_smem = x_fits(p, p->cluster_dyn_smem);
@@ -308,6 +314,7 @@ void launch_engine(pt_plan* p, const KernelSet& ks, const pt_step_params& sp, co
   }
   DevPlan dp = p->dp;
   dp.mgs_smem = p->grid_dyn_smem > 0;
+  dp.dyn_smem = dp.mgs_smem;
   dp.mgs_warp = p->grid_warp;
   dp.bs_smem = stage_fits(p, p->grid_dyn_smem);
   dp.x_smem = x_fits(p, p->grid_dyn_smem);
@@ -409,7 +416,8 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
         {hp.bundles.data(), hp.bundles.size() * sizeof(ptplan::Bundle)},
         {hp.btasks.data(), hp.btasks.size() * sizeof(ptplan::SlotTask)},
         {hp.s_ws.data(), hp.s_ws.size() * 4},
-        {hp.s_coef.data(), hp.s_coef.size() * 8}};
+        {hp.s_coef.data(), hp.s_coef.size() * 8},
+        {hp.splits.data(), hp.splits.size() * 4}};
     size_t total = 0;
     std::vector<size_t> offs;
     for (auto& pc : pieces) {
@@ -444,9 +452,11 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     p->tasks_b = (const ptplan::SlotTask*)(base + offs[11]);
     for (int c = 0; c < 6; ++c) p->class_beg_b[c] = hp.class_beg_b[c];
     if (!hp.bundles.empty()) {
-      static_assert(ptplan::kBundleWarps == kWarps, "bundles are dealt to the warps of a batch CTA");
       p->bundles = (const ptplan::Bundle*)(base + offs[12]);
-      for (int w = 0; w <= kWarps; ++w) p->bundle_warp_beg[w] = hp.bundle_warp_beg[w];
+      p->n_bundles = (int)hp.bundles.size();
+      p->splits = (const int32_t*)(base + offs[16]);
+      p->n_splits = (int)(hp.splits.size() / 4);
+      p->scratch_units = hp.scratch_units;
       p->btasks = (const ptplan::SlotTask*)(base + offs[13]);
       p->s_ws = (const int32_t*)(base + offs[14]);
       p->s_coef = (const double*)(base + offs[15]);
@@ -509,6 +519,7 @@ int64_t pt_plan_info(const pt_plan* p, int32_t what) {
     case 7: return p->dp.ws_len;
     case 8: return p->engine;
     case 9: return p->cluster_size;
+    case 10: return p->batch_threads;
   }
   return -1;
 }
@@ -712,6 +723,8 @@ static int ensure_batch(pt_plan* p) {
   int per_sm = 0, sms = 0;
   const void* fn = kset(p->prec).track_batch;
   p->batch_dyn_smem = engine_smem(p->L, p->N, p->n, 1, true, &p->batch_warp);
+  // split-bundle scratch (eval_bundles) after the x copy in the dynamic smem
+  const size_t scratch_end = (((size_t)2 * p->L * p->n + 31) & ~(size_t)31) + (size_t)p->scratch_units * 32 * 2 * p->L;
   const char* be = getenv("PT_MGS_BATCH");  // tuning knob: 0 keeps the warp / group MGS in the batch
   p->batch_mgs = (p->N <= kBmMaxN && !(be && be[0] == '0')) ? 1 : 0;
   if (p->batch_mgs) {  // the padded matrix, then (after the MGS) the staged R and the x copy reuse it
@@ -719,12 +732,14 @@ static int ensure_batch(pt_plan* p) {
     p->batch_dyn_smem = std::max({bm_smem_doubles(p->L, p->N, p->n), backsub_stage_doubles(p->L, p->n),
                                   (size_t)2 * p->L * p->n}) * 8;
   }
+  p->batch_mgs_smem = p->batch_dyn_smem > 0;  // before the x copy / split scratch may enlarge it
+  p->batch_dyn_smem = std::max(p->batch_dyn_smem, scratch_end * 8);
   int rc = set_dyn_smem(fn, p->batch_dyn_smem);
   if (rc) return rc;
   cudaDeviceProp prop;
   PT_CUDA(cudaGetDeviceProperties(&prop, p->device));
   sms = prop.multiProcessorCount;
-  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, p->batch_dyn_smem));
+  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->batch_threads, p->batch_dyn_smem));
   p->batch_blocks = std::max(1, per_sm) * sms;
   p->bwork = dev_alloc<double>((size_t)p->lay.dslice * p->batch_blocks, &rc);
   if (rc) return rc;
@@ -748,12 +763,15 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
   PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 16, s));
-  rc = set_dyn_smem(tset(p).track_batch, p->batch_dyn_smem);  // per-function attribute: this plan's value
+  const void* fn_fast = tset(p).track_batch;
+  const void* fn_exact = tset_exact(p).track_batch;
+  rc = set_dyn_smem(fn_fast, p->batch_dyn_smem);  // per-function attribute: this plan's value
   if (rc) return rc;
   const unsigned long long epoch = (++p->launches) << 40;
   const int blocks = std::min(p->batch_blocks, n_paths);
   DevPlan bdp = p->dp;
-  bdp.mgs_smem = p->batch_dyn_smem > 0;
+  bdp.mgs_smem = p->batch_mgs_smem;
+  bdp.dyn_smem = p->batch_dyn_smem > 0;
   bdp.mgs_warp = p->batch_warp;
   bdp.mgs_batch = p->batch_mgs;
   bdp.bs_smem = stage_fits(p, p->batch_dyn_smem);
@@ -761,7 +779,10 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   bdp.tasks = p->tasks_b;
   for (int c = 0; c < 6; ++c) bdp.class_beg[c] = p->class_beg_b[c];
   bdp.bundles = p->bundles;
-  for (int w = 0; w <= kWarps; ++w) bdp.bundle_warp_beg[w] = p->bundle_warp_beg[w];
+  bdp.n_bundles = p->n_bundles;
+  bdp.splits = p->splits;
+  bdp.n_splits = p->n_splits;
+  bdp.scratch_units = p->scratch_units;
   bdp.btasks = p->btasks;
   bdp.s_ws = p->s_ws;
   bdp.s_coef = p->s_coef;
@@ -774,16 +795,16 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   unsigned long long ep = epoch;
   int retrack = 0;
   void* args[] = {&bdp, &p->bwork, &p->bu, &lay, &spc, &d_starts, &d_ends, &d_stats, &np, &p->d_queue, &ep, &retrack};
-  PT_CUDA(launch_ex(tset(p).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
-  if (&tset_exact(p) != &tset(p)) {
+  PT_CUDA(launch_ex(fn_fast, blocks, p->batch_dyn_smem, s, 1, args, p->batch_threads));
+  if (fn_exact != fn_fast) {
     // exact re-track of the paths whose fast run met a non-finite value
     // (PT_STAT_NONFINITE): the queue restarts, the abort word is kept
     PT_CUDA(cudaMemsetAsync(p->d_queue, 0, 8, s));
-    rc = set_dyn_smem(tset_exact(p).track_batch, p->batch_dyn_smem);
+    rc = set_dyn_smem(fn_exact, p->batch_dyn_smem);
     if (rc) return rc;
     retrack = 1;
     ep = (++p->launches) << 40;
-    PT_CUDA(launch_ex(tset_exact(p).track_batch, blocks, p->batch_dyn_smem, s, 1, args));
+    PT_CUDA(launch_ex(fn_exact, blocks, p->batch_dyn_smem, s, 1, args, p->batch_threads));
   }
   PT_CUDA(cudaGetLastError());
   return PT_OK;

@@ -266,3 +266,20 @@ def test_batch_kernel_tiny_systems_bitwise(gpu, orc, n):
     for p, (o, s) in enumerate(zip(outs, st_ref)):
         assert (o.success, o.steps, o.newton_iters, o.solves) == (s.status == 0, s.steps, s.newton_iters, s.solves), p
     assert_bits_equal_nan(ends, ends_ref, "end points")
+
+
+@pytest.mark.parametrize("prec", [PM.DD, PM.D])
+def test_batch_split_bundles_bitwise(gpu, orc, prec):
+    """Long slot sums split over D lanes (the value slot: K = 1501, width 128,
+    D = 8; the Jacobian slots: K ~ 375, width 32, D = 4) and merged after the
+    bundle pass -- bitwise against the oracle and the unbundled kernel."""
+    w = W.random_system(n=16, degree=4, n_monomials=1500, prec=prec, seed=31, n_paths=8)
+    w.params.max_steps = 3
+    hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)
+    ends, outs = hom.track_batch(w.starts, w.params)
+    ends_ref, st_ref = orc.track_batch(int(w.prec), w.g, w.f, w.gamma, w.k, w.starts, w.params, THREADS)
+    for p, (o, s) in enumerate(zip(outs, st_ref)):
+        assert (o.success, o.steps, o.newton_iters, o.solves) == (s.status == 0, s.steps, s.newton_iters, s.solves), p
+        assert_bits_equal_nan(np.array([o.final_residual, o.final_update]),
+                              np.array([s.final_residual, s.final_update]), f"stats of path {p}")
+    assert_bits_equal_nan(ends, ends_ref, "end points")
