@@ -725,8 +725,11 @@ static int ensure_batch(pt_plan* p) {
   p->batch_dyn_smem = engine_smem(p->L, p->N, p->n, 1, true, &p->batch_warp);
   // split-bundle scratch (eval_bundles) after the x copy in the dynamic smem
   const size_t scratch_end = (((size_t)2 * p->L * p->n + 31) & ~(size_t)31) + (size_t)p->scratch_units * 32 * 2 * p->L;
-  const char* be = getenv("PT_MGS_BATCH");  // tuning knob: 0 keeps the warp / group MGS in the batch
-  p->batch_mgs = (p->N <= kBmMaxN && !(be && be[0] == '0')) ? 1 : 0;
+  // PT_MGS_BATCH=1: the column-item MGS (mgs_batch.cuh) instead of the warp MGS.
+  // Measured on C5 (same box, A/B x2): warp MGS 8.11 s, column items 8.51 s
+  // per 2368 paths -- the warp MGS stays the default.
+  const char* be = getenv("PT_MGS_BATCH");
+  p->batch_mgs = (p->N <= kBmMaxN && be && be[0] == '1') ? 1 : 0;
   if (p->batch_mgs) {  // the padded matrix, then (after the MGS) the staged R and the x copy reuse it
     p->batch_warp = 0;
     p->batch_dyn_smem = std::max({bm_smem_doubles(p->L, p->N, p->n), backsub_stage_doubles(p->L, p->n),
