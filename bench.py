@@ -9,7 +9,7 @@ double-double -- the workload that shards across GPUs.
                   [--workload batch32|chandra64|cyclic16|rand96|cyclic256] [--prec d|dd|qd]
 
 A step (batch) is one k_track_batch launch over a fixed slice of
---paths-per-step (2048) paths per rank: at step s rank r tracks paths
+--paths-per-step (4096, half the batch) paths per rank: at step s rank r tracks paths
 [((s N + r) P) mod 8192, +P) (multi.step_slice) -- weak scaling, N ranks
 cover N slices per step, no collective on the data path.  A step
 (single-path workloads) is one tracked path; at N > 1 each rank tracks a
@@ -51,12 +51,14 @@ BATCH_METRIC = "paths/sec/box; batch of 8192 dim-32 random degree-4 paths (M=512
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="batch32")
     ap.add_argument("--prec", default=None)
-    ap.add_argument("--paths-per-step", type=int, default=2048, help="batch: paths per rank per step")
+    # 4096: the launch tail (the last long paths of a launch, ~1.5 s) costs 4 % of a
+    # 13 s step; 2048 / 4096 / 8192 measured 295 / 308 / 316 paths/s (profiles/r02)
+    ap.add_argument("--paths-per-step", type=int, default=4096, help="batch: paths per rank per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-paths", type=int, default=96, help="batch: CPU sample paths per reference step")

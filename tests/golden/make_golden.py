@@ -28,13 +28,16 @@ ALL_OPS = ["add", "sub", "mul", "mul_d", "div", "sqrt", "renorm", "cmul", "cadd"
            "modulus_double", "powi", "cscale", "cpowi"]
 
 TRACKS = [("cyclic16", pt.PrecisionMode.DD), ("cyclic16", pt.PrecisionMode.D), ("chandra64", pt.PrecisionMode.D),
-          ("chandra64", pt.PrecisionMode.DD)]
+          ("chandra64", pt.PrecisionMode.DD), ("cyclic16", pt.PrecisionMode.QD), ("chandra64", pt.PrecisionMode.QD)]
 
 
-def main():
+def main(tracks_only=False):
+    """tracks_only (argv "--tracks"): regenerate the track fixtures only."""
     ref = Oracle("reference")
     assert ref.variant == "reference"
     for prec, tag in enumerate(("d", "dd", "qd")):
+        if tracks_only:
+            break
         blob = {}
         for op in ALL_OPS:
             a = random_operands(prec, 256, 101, positive=(op == "sqrt"), oracle=ref)
@@ -56,4 +59,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(tracks_only="--tracks" in sys.argv)

@@ -23,7 +23,7 @@ def _gamma(z, prec):
 
 
 @pytest.mark.parametrize("name,prec", [("cyclic16", PM.DD), ("cyclic16", PM.D), ("chandra64", PM.D),
-                                       ("chandra64", PM.DD)])
+                                       ("chandra64", PM.DD), ("cyclic16", PM.QD), ("chandra64", PM.QD)])
 def test_restatement_tracker_matches_reference_build(oracle, ref_oracle, name, prec):
     w = W.by_name(name, prec)
     e1, s1, t1 = oracle.track_path(int(prec), w.g, w.f, w.gamma, w.k, w.start, w.params, 600)
@@ -34,7 +34,7 @@ def test_restatement_tracker_matches_reference_build(oracle, ref_oracle, name, p
 
 
 @pytest.mark.parametrize("name,prec", [("cyclic16", PM.DD), ("cyclic16", PM.D), ("chandra64", PM.D),
-                                       ("chandra64", PM.DD)])
+                                       ("chandra64", PM.DD), ("cyclic16", PM.QD), ("chandra64", PM.QD)])
 def test_golden_tracks(oracle, name, prec):
     g = np.load(os.path.join(GOLDEN, f"track_{name}_{prec.name.lower()}.npz"))
     w = W.by_name(name, prec)

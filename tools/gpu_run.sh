@@ -1,3 +1,6 @@
-O=gpurun_out/r02s16; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_parity.py tests/test_monodromy.py -q -m gpu -x -p no:cacheprovider > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
-for u in 1 0 1 0; do PT_UNIFORM=$u timeout 300 python tools/prof_batch.py dd 2368 > $O/prof_u$u.json 2>&1; echo "u$u $(cat $O/prof_u$u.json)"; done
+O=gpurun_out/r02s18; mkdir -p $O
+timeout 600 python -m pytest tests/test_qdfast.py -q -m gpu -p no:cacheprovider 2>&1 | tail -2
+for e in 0 1; do
+  PT_ENGINE=$e timeout 600 python bench.py --workload chandra64 --prec qd --arith fast --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_qdfast_e$e.json 2> $O/err_$e.txt
+  python -c "import json; d=json.loads(open('$O/bench_qdfast_e$e.json').read().strip().splitlines()[-1]); print('engine$e', round(d['ms_per_step'],2), d.get('critical_path',{}).get('ns_per_column_step'), d.get('phases_ms'))" || tail -3 $O/err_$e.txt
+done
