@@ -83,6 +83,7 @@ struct DevPlan {
   const int32_t* s_ws;
   const double* s_coef;
   long s_len;
+  int s_hi;  // the stream holds only the leading limb of re / im (the others are +0.0)
 };
 
 // One path's workspace.  All arrays are complex SoA unless noted.
@@ -802,7 +803,13 @@ __device__ __forceinline__ cplx<R> lane_canon32(const DevPlan& P, const Work& W,
 template <class R>
 __device__ __forceinline__ cplx<R> s_contrib(const DevPlan& P, const Work& W, long at) {
   const int wi = P.s_ws[at];
-  const cplx<R> c = load_c<R>(P.s_coef, P.s_len * 32, at);
+  cplx<R> c;
+  if (P.s_hi) {  // binary64 coefficients: rebuild the +0.0 lower limbs (same operand bits)
+    c.re = r_from(P.s_coef[at], static_cast<R*>(nullptr));
+    c.im = r_from(P.s_coef[P.s_len * 32 + at], static_cast<R*>(nullptr));
+  } else {
+    c = load_c<R>(P.s_coef, P.s_len * 32, at);
+  }
   const cplx<R> m = load_c<R>(W.ws, P.ws_len, wi < 0 ? 0 : wi);
   return pick(wi < 0, c, c_mul(c, m));
 }

@@ -105,7 +105,9 @@ struct HostPlan {
   int32_t scratch_units = 0;              // 32-lane complex rows of split scratch
   std::vector<SlotTask> btasks;           // lane tasks in bundle order
   std::vector<int32_t> s_ws;              // [s_len][32] workspace index (-1: constant term)
-  std::vector<double> s_coef;             // [2L][s_len * 32] coefficient limbs
+  std::vector<double> s_coef;             // [2L][s_len * 32] coefficient limbs ([2][..] when s_hi)
+  int32_t s_hi = 0;                       // every streamed coefficient has +0.0 lower limbs: only
+                                          // the leading limb of re / im is stored (half the bytes)
   int64_t s_len = 0;
   // coefficients of all terms of g then f, complex SoA [2][L][n_coef]
   std::vector<double> coef;
@@ -202,14 +204,32 @@ inline void build_bundles(HostPlan& P) {
   if (len > kStreamCap) return;
   P.s_len = std::max<int64_t>(len, 1);
   const int64_t S = P.s_len * 32;
+  // coefficients built from binary64 values (random / integer systems): the
+  // lower limbs are exactly +0.0 (bit pattern 0), so the device rebuilds them
+  // from the leading limb alone -- the same operands, half the stream
+  const char* he = std::getenv("PT_STREAM_HI");  // tuning knob: 0 keeps every limb
+  bool hi = L > 1 && !(he && he[0] == '0');
+  for (int64_t t = 0; hi && t < P.n_coef; ++t)
+    for (int q = 0; q < 2 * L && hi; ++q) {
+      if (q % L == 0) continue;
+      const double v = P.coef[(size_t)q * P.n_coef + t];
+      uint64_t bits;
+      std::memcpy(&bits, &v, 8);
+      hi = bits == 0;
+    }
+  P.s_hi = hi ? 1 : 0;
+  const int planes = hi ? 2 : 2 * L;
   P.s_ws.assign((size_t)S, 0);
-  P.s_coef.assign((size_t)2 * L * S, 0.0);
+  P.s_coef.assign((size_t)planes * S, 0.0);
   auto fill = [&](int64_t row, int lane, int32_t beg, int32_t cnt) {
     for (int32_t r = 0; r < cnt; ++r) {
       const int64_t at = (row + r) * 32 + lane;
       const int32_t ci = P.ctr_coef[beg + r];
       P.s_ws[at] = P.ctr_ws[beg + r];
-      for (int q = 0; q < 2 * L; ++q) P.s_coef[(size_t)q * S + at] = P.coef[(size_t)q * P.n_coef + ci];
+      for (int q = 0; q < planes; ++q) {
+        const int src = hi ? q * L : q;  // leading limb of re (q = 0) / im (q = 1)
+        P.s_coef[(size_t)q * S + at] = P.coef[(size_t)src * P.n_coef + ci];
+      }
     }
   };
   for (const Bundle& B : bs) {

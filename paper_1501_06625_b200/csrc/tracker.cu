@@ -91,6 +91,7 @@ struct pt_plan {
   const int32_t* s_ws = nullptr;
   const double* s_coef = nullptr;
   long s_len = 0;
+  int s_hi = 0;
   int arith = 0;              // PT_ARITH_REFERENCE / PT_ARITH_FAST (QD only)
   int engine = 0;             // 0 grid, 1 cluster (single path)
   int cluster_size = 0;       // CTAs of the cluster engine (0: unavailable)
@@ -461,6 +462,7 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
       p->s_ws = (const int32_t*)(base + offs[14]);
       p->s_coef = (const double*)(base + offs[15]);
       p->s_len = (long)hp.s_len;
+      p->s_hi = hp.s_hi;
     }
     dp.ctr_coef = (const int32_t*)(base + offs[7]);
     dp.ctr_ws = (const int32_t*)(base + offs[8]);
@@ -790,6 +792,7 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   bdp.s_ws = p->s_ws;
   bdp.s_coef = p->s_coef;
   bdp.s_len = p->s_len;
+  bdp.s_hi = p->s_hi;
   // launched as clusters of one CTA: the warp MGS pushes q_k with st.async,
   // which needs a cluster launch even when the cluster is the CTA itself
   Layout lay = p->lay;

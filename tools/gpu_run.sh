@@ -1,6 +1,3 @@
-O=gpurun_out/r02s18; mkdir -p $O
-timeout 600 python -m pytest tests/test_qdfast.py -q -m gpu -p no:cacheprovider 2>&1 | tail -2
-for e in 0 1; do
-  PT_ENGINE=$e timeout 600 python bench.py --workload chandra64 --prec qd --arith fast --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_qdfast_e$e.json 2> $O/err_$e.txt
-  python -c "import json; d=json.loads(open('$O/bench_qdfast_e$e.json').read().strip().splitlines()[-1]); print('engine$e', round(d['ms_per_step'],2), d.get('critical_path',{}).get('ns_per_column_step'), d.get('phases_ms'))" || tail -3 $O/err_$e.txt
-done
+O=gpurun_out/r02s19; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_configs.py -q -m gpu -x -p no:cacheprovider -k "batch" > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
+for h in 1 0 1 0; do PT_STREAM_HI=$h timeout 300 python tools/prof_batch.py dd 2368 > $O/prof_h$h.json 2>&1; echo "h$h $(cat $O/prof_h$h.json)"; done
