@@ -108,8 +108,15 @@ __device__ void cta_prologue(const DevPlan& P, Smem<R>& sh, double* dyn_smem, in
   }
 }
 
+// CTAs per SM of the cooperative grid engine (k_track_grid, k_eval): two in
+// D / DD (128 registers, twice the warps to hide the L2 latency of the slot
+// sums: rand-96 DD evaluation 1.03 -> 0.90 ms, a 3-step prefix 39.5 -> 34.2
+// ms), one in QD (at 128 registers the QD chains spill: cyclic-256 QD
+// evaluation 19.4 -> 24.7 ms).
 template <class R>
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kGridCtasPerSm = limbs_of<R>::L == 4 ? 1 : 2;
+template <class R>
+__global__ void __launch_bounds__(kThreads, kGridCtasPerSm<R>)
     k_track_grid(DevPlan P, Work W, pt_step_params sp, TrackIO io, unsigned long long epoch_base) {
   __shared__ Smem<R> sh;
   extern __shared__ double dyn_smem[];
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, kBatchCtasPerSm<R>)
 }
 
 template <class R>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kGridCtasPerSm<R>)
     k_eval(DevPlan P, Work W, const double* x, double t, double* h, double* J, double* rmax) {
   __shared__ Smem<R> sh;
   const GridTeam team{W.ctl, (int)gridDim.x, (int)blockIdx.x, nullptr};

@@ -199,16 +199,23 @@ int dispatch_grid_size(pt_plan* p) {
   want = std::max(want, (long)(p->M + kThreads - 1) / kThreads);
   want = std::max(want, (ntasks + kWarps - 1) / kWarps);
   want = std::max(want, (long)(p->n + 1 + gpc_mgs - 1) / gpc_mgs);
-  p->grid_blocks = (int)std::min<long>(want, std::min(cap, sms));
-  p->grid_dyn_smem = engine_smem(p->L, p->N, p->n, p->grid_blocks, false, &p->grid_warp);
-  for (const void* f : {fn, kset_exact(p->prec).eval}) {
-    rc = set_dyn_smem(f, p->grid_dyn_smem);
-    if (rc) return rc;
+  // cap = resident CTAs without dynamic smem (kGridCtasPerSm per SM); the
+  // cooperative launch needs every CTA resident WITH the MGS staging, so the
+  // grid shrinks until the occupancy at that staging size covers it
+  p->grid_blocks = (int)std::min<long>(want, cap);
+  for (int round = 0;; ++round) {
+    p->grid_dyn_smem = engine_smem(p->L, p->N, p->n, p->grid_blocks, false, &p->grid_warp);
+    for (const void* f : {fn, kset_exact(p->prec).eval}) {
+      rc = set_dyn_smem(f, p->grid_dyn_smem);
+      if (rc) return rc;
+    }
+    int per_sm2 = 0;
+    PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, fn, kThreads, p->grid_dyn_smem));
+    if (per_sm2 < 1) return fail(PT_E_INVAL, "tracker CTA does not fit on an SM");
+    if (per_sm2 * sms >= p->grid_blocks) return PT_OK;
+    if (round >= 4) return fail(PT_E_INVAL, "grid engine: no co-resident grid size found");
+    p->grid_blocks = per_sm2 * sms;
   }
-  int per_sm2 = 0;
-  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, fn, kThreads, p->grid_dyn_smem));
-  if (per_sm2 < 1) return fail(PT_E_INVAL, "tracker CTA does not fit on an SM");
-  return PT_OK;
 }
 
 // Largest cluster (<= 16 CTAs) the device can schedule for this kernel with

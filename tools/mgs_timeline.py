@@ -1,5 +1,5 @@
 """Per-column MGS timeline of the last tracked path (pt_plan_mgs_timeline):
-python tools/mgs_timeline.py <workload> <prec> [engine]"""
+python tools/mgs_timeline.py <workload> <prec> [engine] [arith]"""
 import json
 import os
 import sys
@@ -15,6 +15,8 @@ w = W.by_name(name, pt.PrecisionMode.parse(prec))
 hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k)
 if len(sys.argv) > 3:
     hom.set_engine(sys.argv[3])
+if len(sys.argv) > 4:
+    hom.set_arith(sys.argv[4])
 for _ in range(2):
     hom.track_path(w.start, w.params)
 n = w.n
