@@ -398,9 +398,9 @@ def run_ours(args):
         for _, t in stats_all:
             raw = t.cpu().numpy()
             stats_list.extend(nat.PathStats.from_buffer_copy(raw[p].tobytes()) for p in range(P))
-    else:
+    else:  # every step tracks the same path: identical statistics per launch
         raw = d_stats.cpu().numpy()
-        stats_list = [nat.PathStats.from_buffer_copy(raw[0].tobytes())]
+        stats_list = [nat.PathStats.from_buffer_copy(raw[0].tobytes())] * args.steps
 
     # e2e through the public C-ABI with pinned host buffers (H2D starts, D2H ends + stats per step)
     h_starts = torch.from_numpy(np.ascontiguousarray(w.starts if batch else w.starts[:1])).pin_memory()
@@ -441,7 +441,11 @@ def run_ours(args):
         tr_path = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr_path):
             with open(tr_path) as fh:
-                traffic = json.load(fh).get(w.name)
+                tr = json.load(fh)
+            # single paths: bytes per launch; the batch: bytes per path x paths per launch
+            traffic = tr.get(w.name)
+            if traffic is None and batch and f"{w.name}/path" in tr:
+                traffic = tr[f"{w.name}/path"] * P
         ok = [s.status == 0 for s in stats_list]
         line = {
             "metric": metric_of(args, w),
