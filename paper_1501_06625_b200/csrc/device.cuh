@@ -800,11 +800,11 @@ __device__ __forceinline__ cplx<R> lane_canon32(const DevPlan& P, const Work& W,
 // = pos*32 + lane.  The index and the 2L coefficient limbs are coalesced
 // across the warp; the workspace entry is the same for every lane when the
 // bundle's slots share their support (a broadcast).
-template <class R>
+template <class R, bool HI>
 __device__ __forceinline__ cplx<R> s_contrib(const DevPlan& P, const Work& W, long at) {
   const int wi = P.s_ws[at];
   cplx<R> c;
-  if (P.s_hi) {  // binary64 coefficients: rebuild the +0.0 lower limbs (same operand bits)
+  if constexpr (HI) {  // binary64 coefficients: rebuild the +0.0 lower limbs (same operand bits)
     c.re = r_from(P.s_coef[at], static_cast<R*>(nullptr));
     c.im = r_from(P.s_coef[P.s_len * 32 + at], static_cast<R*>(nullptr));
   } else {
@@ -815,13 +815,15 @@ __device__ __forceinline__ cplx<R> s_contrib(const DevPlan& P, const Work& W, lo
 }
 
 // lane_canon32 over a stream (contribution r of this lane at (s0 + r)*32 + lane).
-template <class R>
+// HI: the stream holds only the leading limb of re / im (DevPlan::s_hi) --
+// a template parameter, not a branch in the loop (the branch cost registers
+// and spills in the hot loop: 11 % on C5).
+template <class R, bool HI>
 __device__ __forceinline__ cplx<R> lane_tree_s(const DevPlan& P, const Work& W, long s0, int lane, int K, int D,
                                                int c) {
   return lane_tree_g<R>(K, K > 0 ? width_eval_d(K) : 32, D, c,
-                        [&](int r) { return s_contrib<R>(P, W, (s0 + r) * 32 + lane); });
+                        [&](int r) { return s_contrib<R, HI>(P, W, (s0 + r) * 32 + lane); });
 }
-
 
 template <class R>
 __device__ __forceinline__ void slot_store(const DevPlan& P, const Work& W, const ptplan::SlotTask& tk,
@@ -850,7 +852,7 @@ __device__ __forceinline__ void slot_store(const DevPlan& P, const Work& W, cons
 // parks it in shared scratch; after one CTA barrier the D subtrees of each
 // split group are merged (tree_combine) and stored.  Own register-allocation
 // unit; one copy of the tree for g and f (instruction cache).
-template <class R>
+template <class R, bool HI>
 __device__ __noinline__ void eval_bundles(const DevPlan& P, const Work& W, const cplx<R> wS, const R wT, int* next,
                                           double* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -869,7 +871,7 @@ __device__ __noinline__ void eval_bundles(const DevPlan& P, const Work& W, const
 #pragma unroll 1
       for (int side = 0; side < 2; ++side) {
         const int K = side ? tk.f_cnt : tk.g_cnt;
-        const cplx<R> v = lane_tree_s<R>(P, W, side ? B.sf : B.sg, lane, K, D, c);
+        const cplx<R> v = lane_tree_s<R, HI>(P, W, side ? B.sf : B.sg, lane, K, D, c);
         if (side)
           Sf = v;
         else
@@ -927,7 +929,10 @@ __device__ __noinline__ void eval_slots(const DevPlan& P, const Work& W, const T
   weights<R>(P, t, wS, wT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (P.bundles != nullptr) {  // batch: lane tasks in warp bundles over coalesced streams
-    eval_bundles<R>(P, W, wS, wT, &sh.bundle_next, scratch);
+    if (P.s_hi)
+      eval_bundles<R, true>(P, W, wS, wT, &sh.bundle_next, scratch);
+    else
+      eval_bundles<R, false>(P, W, wS, wT, &sh.bundle_next, scratch);
   } else {  // lane tasks: one slot per lane (canonical width 32, K <= lane_k)
     constexpr int KM = limbs_of<R>::L == 4 ? 4 : 8;
     const int beg = P.class_beg[0], end = P.class_beg[1];
