@@ -221,13 +221,18 @@ def test_finite_paths_are_not_flagged(gpu):
 # N <= 64: one and two elements per leaf, partial and full items), each
 # against the unbundled / warp-MGS variants and the oracle.  Short prefixes
 # keep the CPU oracle fast; every counter, residual and end point bitwise.
-@pytest.mark.parametrize("variant", ["new", "old"])
+@pytest.mark.parametrize("variant", ["new", "old", "allimbs"])
 @pytest.mark.parametrize("n,prec", [(5, PM.D), (12, PM.DD), (32, PM.QD), (40, PM.DD), (64, PM.D), (48, PM.QD),
                                     (64, PM.DD)])
 def test_batch_kernel_shapes_bitwise(gpu, orc, monkeypatch, n, prec, variant):
-    flag = "1" if variant == "new" else "0"
+    """new: bundles + column-item MGS; old: unbundled lane / group sums + warp
+    MGS; allimbs: bundles whose streams keep every coefficient limb (the
+    random coefficients are binary64, so by default only the leading limbs
+    are streamed)."""
+    flag = "0" if variant == "old" else "1"
     monkeypatch.setenv("PT_BUNDLES", flag)
     monkeypatch.setenv("PT_MGS_BATCH", flag)
+    monkeypatch.setenv("PT_STREAM_HI", "0" if variant == "allimbs" else "1")
     w = W.random_system(n=n, degree=2, n_monomials=3 * n, prec=prec, seed=100 + n, n_paths=12)
     w.params.max_steps = 4
     hom = pt.make_homotopy(w.g, w.f, w.gamma, w.k, device=gpu)

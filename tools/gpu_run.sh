@@ -1,6 +1,8 @@
-O=gpurun_out/r02ab2; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_configs.py -q -m gpu -x -p no:cacheprovider -k "batch" > $O/pytest.log 2>&1; tail -1 $O/pytest.log
-for v in cur old hi0 cur old hi0; do
-  case $v in old) export PT_LIB_PATH=$PWD/tools/lib_0287fce.so; unset PT_STREAM_HI;; hi0) unset PT_LIB_PATH; export PT_STREAM_HI=0;; *) unset PT_LIB_PATH PT_STREAM_HI;; esac
-  timeout 300 python tools/prof_batch.py dd 2368 > $O/prof_$v.json 2>&1; echo "$v $(cat $O/prof_$v.json)"
+# round-2 headline: default bench (C5) twice + reference arm
+O=gpurun_out/r02head; mkdir -p $O
+for i in 1 2; do
+  timeout 1200 python bench.py > $O/bench_batch32_dd_$i.json 2> $O/bench_batch32_dd_$i.err
+  python -c "import json; d=json.loads(open('$O/bench_batch32_dd_$i.json').read().strip().splitlines()[-1]); print('batch', round(d['value'],1), round(d['ms_per_step'],1), round(d['e2e']['value'],1), round(d['roofline']['frac'],4), d['clocks'])"
 done
+timeout 1200 python bench.py --paths-per-step 8192 --steps 2 --warmup 1 --no-cpu-baseline > $O/bench_batch32_dd_pp8192.json 2>&1
+python -c "import json; d=json.loads(open('$O/bench_batch32_dd_pp8192.json').read().strip().splitlines()[-1]); print('batch pp8192', round(d['value'],1))"
