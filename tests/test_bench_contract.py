@@ -64,6 +64,10 @@ def test_our_arm_contract(gpu):
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= r.keys() and 0 < r["frac"] < 1
+    # achieved = the algorithmic work of ONE launch (one tracked path) over the launch time
+    per_launch = r["work_per_launch_fp64_instr"] / (d["ms_per_step"] * 1e-3) / 1e12
+    assert abs(r["achieved"] - per_launch) <= 0.05 * per_launch, (r["achieved"], per_launch)
+    assert r["work_per_launch_fp64_instr"] > d["path"]["newton_iters"] * r["work_per_eval"]
     assert d["gpu_launches"] == 2
     assert d["path"]["success"]
     assert d["critical_path"]["columns_per_solve"] == 64
