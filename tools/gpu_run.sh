@@ -1,8 +1,6 @@
-# round-2 headline: default bench (C5) twice + reference arm
-O=gpurun_out/r02head; mkdir -p $O
-for i in 1 2; do
-  timeout 1200 python bench.py > $O/bench_batch32_dd_$i.json 2> $O/bench_batch32_dd_$i.err
-  python -c "import json; d=json.loads(open('$O/bench_batch32_dd_$i.json').read().strip().splitlines()[-1]); print('batch', round(d['value'],1), round(d['ms_per_step'],1), round(d['e2e']['value'],1), round(d['roofline']['frac'],4), d['clocks'])"
-done
-timeout 1200 python bench.py --paths-per-step 8192 --steps 2 --warmup 1 --no-cpu-baseline > $O/bench_batch32_dd_pp8192.json 2>&1
-python -c "import json; d=json.loads(open('$O/bench_batch32_dd_pp8192.json').read().strip().splitlines()[-1]); print('batch pp8192', round(d['value'],1))"
+O=gpurun_out/r02own; mkdir -p $O
+PT_MGS_OWNERS=4 timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -p no:cacheprovider -k "track" > $O/pytest4.log 2>&1; tail -1 $O/pytest4.log
+for o in 8 4 2; do for wl in "chandra64 dd 20 5" "chandra64 d 20 5" "cyclic16 dd 10 3"; do set -- $wl
+  PT_MGS_OWNERS=$o timeout 600 python bench.py --workload $1 --prec $2 --steps $3 --warmup $4 --no-cpu-baseline > $O/b_$o_$1_$2.json 2>/dev/null
+  python -c "import json; d=json.loads(open('$O/b_$o_$1_$2.json').read().strip().splitlines()[-1]); print('owners$o $1 $2', round(d['ms_per_step'],2), d.get('critical_path',{}).get('ns_per_column_step'))"
+done; done
