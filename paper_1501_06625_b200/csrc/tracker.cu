@@ -164,9 +164,9 @@ size_t mgs_smem_bytes(int L, int N, int n, int nblocks) {
 //   0  group MGS of device.cuh (any N up to 1024).
 // QD keeps the group MGS: its column chain is issue bound, and groups of
 // 2+ warps put one element per thread on it.  PT_MGS_WARP=<0|1|2> caps it.
-size_t engine_smem(int L, int N, int n, int nblocks, bool cluster_or_block, int* warp) {
+size_t engine_smem(int L, int N, int n, int nblocks, bool cluster_or_block, int* warp, int cap_default = 2) {
   const char* e = getenv("PT_MGS_WARP");
-  int cap = e ? atoi(e) : (L == 4 ? 0 : 2);
+  int cap = e ? atoi(e) : (L == 4 ? 0 : cap_default);
   if (!cluster_or_block) cap = std::min(cap, 1);
   *warp = 0;
   if (N <= kWarpMgsMaxN) {
@@ -731,7 +731,11 @@ static int ensure_batch(pt_plan* p) {
   if (p->bwork) return PT_OK;
   int per_sm = 0, sms = 0;
   const void* fn = kset(p->prec).track_batch;
-  p->batch_dyn_smem = engine_smem(p->L, p->N, p->n, 1, true, &p->batch_warp);
+  // batch: the warp MGS hands q_k on through shared memory + flags (mode 1):
+  // one CTA has no remote consumer for the TMA multicast, and without the Q
+  // buffer each CTA leaves 33 KB more of the SM to L1 (C5: 7.30-7.38 s vs
+  // 7.47-7.49 s per 2368 paths, same box)
+  p->batch_dyn_smem = engine_smem(p->L, p->N, p->n, 1, true, &p->batch_warp, 1);
   // split-bundle scratch (eval_bundles) after the x copy in the dynamic smem
   const size_t scratch_end = (((size_t)2 * p->L * p->n + 31) & ~(size_t)31) + (size_t)p->scratch_units * 32 * 2 * p->L;
   // PT_MGS_BATCH=1: the column-item MGS (mgs_batch.cuh) instead of the warp MGS.
