@@ -144,6 +144,36 @@ class Homotopy {
     return o;
   }
 
+  // Many independent paths (one tracker per path), one CTA
+  // per path on the device (pt_track_batch): outcome p belongs to starts[p].
+  std::vector<TrackOutcome<Real>> track_batch(const std::vector<Point<Real>>& starts,
+                                              const pt_step_params* params = nullptr) const {
+    pt_step_params p{};
+    if (!params) {
+      check(pt_default_params(prec_of<Real>(), &p));
+      params = &p;
+    }
+    std::vector<double> in;
+    for (const auto& s : starts) {
+      const std::vector<double> l = to_limbs<Real>(s);
+      in.insert(in.end(), l.begin(), l.end());
+    }
+    std::vector<double> out(in.size());
+    std::vector<pt_path_stats> st(starts.size());
+    if (!starts.empty()) check(pt_track_batch(plan_, (int32_t)starts.size(), in.data(), params, out.data(), st.data()));
+    std::vector<TrackOutcome<Real>> res(starts.size());
+    const size_t per = starts.empty() ? 0 : in.size() / starts.size();
+    for (size_t q = 0; q < starts.size(); ++q) {
+      res[q].stats = st[q];
+      res[q].success = st[q].status == PT_PATH_SUCCESS;
+      res[q].end = from_limbs<Real>(std::vector<double>(out.begin() + q * per, out.begin() + (q + 1) * per), n_);
+    }
+    return res;
+  }
+
+  // QD only: opt into the tolerance-parity arithmetic (pt_plan_set_arith).
+  void set_fast_arithmetic(bool fast) { check(pt_plan_set_arith(plan_, fast ? PT_ARITH_FAST : PT_ARITH_REFERENCE)); }
+
   pt_plan* plan() const { return plan_; }
 
  private:

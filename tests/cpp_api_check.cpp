@@ -33,6 +33,13 @@ int main() {
     b200::Homotopy<R> h(g, f, Complex<R>(R(0.6), R(0.8)), 2);
     auto o = h.track_path(x0);
     std::printf("device: success=%d x=%.17g steps=%d\n", (int)o.success, o.end[0].re.hi, o.stats.steps);
+    // the batch entry: three copies of the start, the same end point bits each time
+    const auto b = h.track_batch(std::vector<Point<R>>(3, x0));
+    for (const auto& ob : b)
+      if (!ob.success || ob.end[0].re.hi != o.end[0].re.hi || ob.end[0].re.lo != o.end[0].re.lo ||
+          ob.stats.steps != o.stats.steps)
+        return 5;
+    std::printf("batch: %zu paths, all equal to the single path\n", b.size());
     return o.success && o.end[0].re.hi == 2.0 ? 0 : 1;
   } catch (const std::runtime_error& e) {
     std::printf("no device: %s\n", e.what());

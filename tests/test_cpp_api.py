@@ -42,3 +42,4 @@ def test_cpp_adapter_tracks_on_device(tmp_path, gpu):
     has no /root/reference)."""
     r = _build_and_run(tmp_path, os.path.isdir(REF_INC))
     assert r.returncode == 0 and "device: success=1" in r.stdout, r.stdout + r.stderr
+    assert "batch: 3 paths, all equal to the single path" in r.stdout, r.stdout
