@@ -126,3 +126,27 @@ def test_error_bounds_vs_bigfloat(oracle, prec, bound, op):
         worst = max(worst, float(abs((got - exact) / exact)))
     assert worst <= lim, (op, worst, lim)
     assert L > 1
+
+
+def test_glibc_hypot_replay_matches_the_host_libm():
+    """modulus_double (complex.hpp:113-116) calls std::hypot, which glibc does
+    not round correctly; the device replays glibc's kernel (mp.cuh
+    glibc_hypot).  Its host build (the same source) against this host's libm
+    (numpy.hypot) on 4e6 pairs: random mantissas with exponents over the
+    whole range (the 2^511 / 2^-459 scaling branches, subnormals), signs
+    mixed, plus ties and exact cases -- bit for bit."""
+    import paper_1501_06625_b200 as pt
+    rng = np.random.default_rng(2024)
+    n = 4_000_000
+    e1 = rng.integers(-1070, 1020, n)
+    e2 = np.clip(e1 + rng.integers(-60, 61, n), -1074, 1023)
+    x = np.ldexp(rng.uniform(0.5, 1.0, n), e1) * rng.choice([-1.0, 1.0], n)
+    y = np.ldexp(rng.uniform(0.5, 1.0, n), e2) * rng.choice([-1.0, 1.0], n)
+    x[:1000], y[:1000] = 3.0 * np.arange(1000), 4.0 * np.arange(1000)  # exact 3-4-5 cases
+    a = np.zeros((n, 2))
+    a[:, 0], a[:, 1] = x, y
+    out = pt.arith(pt.PrecisionMode.D, 11, a, np.zeros_like(a), device=None)
+    got = out.reshape(n, 2)[:, 0]
+    want = np.hypot(x, y)
+    bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, (bad.size, x[bad[:3]], y[bad[:3]], got[bad[:3]], want[bad[:3]])

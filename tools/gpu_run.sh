@@ -1,4 +1,2 @@
-O=gpurun_out/r02mw1; mkdir -p $O
-timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
-timeout 1200 python bench.py > $O/bench_batch32_dd.json 2> $O/bench_batch32_dd.err
-python -c "import json; d=json.loads(open('$O/bench_batch32_dd.json').read().strip().splitlines()[-1]); print('batch', round(d['value'],1), round(d['ms_per_step'],1), round(d['e2e']['value'],1), round(d['roofline']['frac'],4), d['clocks'])"
+O=gpurun_out/r02cpp; mkdir -p $O
+timeout 600 python -m pytest tests/test_cpp_api.py tests/test_bench_contract.py -q -p no:cacheprovider > $O/pytest.log 2>&1; tail -3 $O/pytest.log
