@@ -140,8 +140,7 @@ void pt_plan_destroy(pt_plan* plan);
 /* Query plan facts: 0 n_vars, 1 n_eqs, 2 monomials, 3 contributions,
  * 4 grid CTAs used for one path, 5 precision, 6 batch CTAs resident,
  * 7 monomial workspace entries, 8 single-path engine (0 grid, 1 cluster),
- * 9 cluster size of the cluster engine (0: none schedulable), 10 threads per
- * batch CTA (128 or 256; valid after the first batch call). */
+ * 9 cluster size of the cluster engine (0: none schedulable). */
 int64_t pt_plan_info(const pt_plan* plan, int32_t what);
 
 /* Force the single-path engine: 0 = cooperative persistent grid (all SMs,

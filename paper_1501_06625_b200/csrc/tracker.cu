@@ -43,11 +43,10 @@ inline const KernelSet& kset_mode(pt_prec p, int arith) { return (p == PT_QD && 
 
 // Launch a kernel (as a cluster of `cluster` CTAs when cluster > 0) from its
 // untyped pointer.
-cudaError_t launch_ex(const void* fn, int grid, size_t smem, cudaStream_t s, int cluster, void** args,
-                      int threads = kThreads) {
+cudaError_t launch_ex(const void* fn, int grid, size_t smem, cudaStream_t s, int cluster, void** args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
+  cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -99,7 +98,6 @@ struct pt_plan {
   size_t batch_dyn_smem = 0;  // dynamic smem of k_track_batch
   int batch_mgs = 0;          // k_track_batch runs mgs_batch (N <= kBmMaxN)
   int batch_mgs_smem = 0;     // the batch's MGS stages its columns in the dynamic smem
-  int batch_threads = kThreads;
   // staging for the host-buffer API
   double* d_start = nullptr;
   double* d_end = nullptr;
@@ -528,7 +526,6 @@ int64_t pt_plan_info(const pt_plan* p, int32_t what) {
     case 7: return p->dp.ws_len;
     case 8: return p->engine;
     case 9: return p->cluster_size;
-    case 10: return p->batch_threads;
   }
   return -1;
 }
@@ -755,7 +752,7 @@ static int ensure_batch(pt_plan* p) {
   cudaDeviceProp prop;
   PT_CUDA(cudaGetDeviceProperties(&prop, p->device));
   sms = prop.multiProcessorCount;
-  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->batch_threads, p->batch_dyn_smem));
+  PT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, p->batch_dyn_smem));
   p->batch_blocks = std::max(1, per_sm) * sms;
   p->bwork = dev_alloc<double>((size_t)p->lay.dslice * p->batch_blocks, &rc);
   if (rc) return rc;
@@ -812,7 +809,7 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
   unsigned long long ep = epoch;
   int retrack = 0;
   void* args[] = {&bdp, &p->bwork, &p->bu, &lay, &spc, &d_starts, &d_ends, &d_stats, &np, &p->d_queue, &ep, &retrack};
-  PT_CUDA(launch_ex(fn_fast, blocks, p->batch_dyn_smem, s, 1, args, p->batch_threads));
+  PT_CUDA(launch_ex(fn_fast, blocks, p->batch_dyn_smem, s, 1, args));
   if (fn_exact != fn_fast) {
     // exact re-track of the paths whose fast run met a non-finite value
     // (PT_STAT_NONFINITE): the queue restarts, the abort word is kept
@@ -821,7 +818,7 @@ int pt_track_batch_device(pt_plan* p, int32_t n_paths, const double* d_starts, c
     if (rc) return rc;
     retrack = 1;
     ep = (++p->launches) << 40;
-    PT_CUDA(launch_ex(fn_exact, blocks, p->batch_dyn_smem, s, 1, args, p->batch_threads));
+    PT_CUDA(launch_ex(fn_exact, blocks, p->batch_dyn_smem, s, 1, args));
   }
   PT_CUDA(cudaGetLastError());
   return PT_OK;
