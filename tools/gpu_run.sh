@@ -1,11 +1,8 @@
-O=gpurun_out/r02p2; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_parity.py tests/test_monodromy.py -q -m gpu -x -p no:cacheprovider > $O/pytest.log 2>&1; tail -1 $O/pytest.log
-for v in cur prev cur prev; do
-  case $v in prev) export PT_LIB_PATH=$PWD/tools/lib_prev.so;; *) unset PT_LIB_PATH;; esac
-  timeout 300 python tools/prof_batch.py dd 2368 > $O/p_$v.json 2>&1; echo "$v $(cat $O/p_$v.json)"
-done
-for v in cur prev; do
-  case $v in prev) export PT_LIB_PATH=$PWD/tools/lib_prev.so;; *) unset PT_LIB_PATH;; esac
-  timeout 600 python bench.py --workload cyclic16 --prec dd --steps 10 --warmup 3 --no-cpu-baseline > $O/c_$v.json 2>/dev/null
-  python -c "import json; d=json.loads(open('$O/c_$v.json').read().strip().splitlines()[-1]); print('cyclic16 dd $v', round(d['ms_per_step'],2))"
-done
+# end-of-round verification: every GPU test, smoke, the default bench line, the reference arm
+O=gpurun_out/r02end; mkdir -p $O
+timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
+timeout 1200 python bench.py > $O/bench_batch32_dd.json 2> $O/bench_batch32_dd.err
+python -c "import json; d=json.loads(open('$O/bench_batch32_dd.json').read().strip().splitlines()[-1]); print('batch', round(d['value'],1), round(d['ms_per_step'],1), round(d['e2e']['value'],1), round(d['roofline']['frac'],4), d['roofline']['traffic'], d['clocks'], d.get('cpu_baseline',{}).get('value'))"
+timeout 1200 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_reference_batch32_dd.json 2> $O/bench_reference.err
+python -c "import json; d=json.loads(open('$O/bench_reference_batch32_dd.json').read().strip().splitlines()[-1]); print('reference', d['value'])"
