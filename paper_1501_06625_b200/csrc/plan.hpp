@@ -86,7 +86,7 @@ struct Bundle {
   int32_t dc;                // D << 8 | c: the lanes sum the subtree c of D (D = 1: the whole slot)
   int32_t split;             // D > 1: scratch row base of the split group (g: base + c, f: base + D + c)
 };
-constexpr int64_t kStreamCap = 64L << 20;  // stream entries (x 32 lanes x (4 + 16L) bytes) before giving up
+constexpr int64_t kStreamCapBytes = 4LL << 30;  // contribution streams larger than this: no bundles
 
 struct HostPlan {
   int n = 0, N = 0, L = 1;
@@ -201,7 +201,7 @@ inline void build_bundles(HostPlan& P) {
       }
     }
   }
-  if (len > kStreamCap) return;
+  if (len * 32 * (4 + 16 * (int64_t)L) > kStreamCapBytes) return;  // the all-limb size bounds the hi-only one
   P.s_len = std::max<int64_t>(len, 1);
   const int64_t S = P.s_len * 32;
   // coefficients built from binary64 values (random / integer systems): the
