@@ -270,23 +270,32 @@ def cpu_single(w, seconds, threads):
 
 def cpu_d_all_cores(args, seconds=2.0):
     """North-star comparison for single paths: the reference CPU tracker in
-    complex DOUBLE on all host cores, same system and prefix (--max-steps)."""
+    complex DOUBLE on the host cores, same system and prefix (--max-steps).
+    The per-path OpenMP of the tracker does not always pay in D (a 64 x 64
+    column sweep is a few microseconds of work per fork), so both 1 thread
+    and all cores are timed and the FASTER one is the baseline."""
     from paper_1501_06625_b200 import PrecisionMode
     a = argparse.Namespace(**vars(args))
     a.prec = "d"
     wd = apply_overrides(a, workload(a))
     orc = _oracle()
-    orc.set_threads(os.cpu_count() or 1)
-    n, iters, t0 = 0, 0, time.perf_counter()
-    while True:
-        _, st, _ = orc.track_path(int(PrecisionMode.D), wd.g, wd.f, wd.gamma, wd.k, wd.start, wd.params)
-        n += 1
-        iters += st.newton_iters
-        if time.perf_counter() - t0 > seconds:
-            break
-    dt = time.perf_counter() - t0
-    return {"sec_per_path": dt / n, "sec_per_newton_iter": dt / max(1, iters), "cores": os.cpu_count() or 1,
-            "paths": n, "newton_iters_per_path": iters / n, "workload": wd.name}
+    best = None
+    for threads in sorted({1, os.cpu_count() or 1}, reverse=True):
+        orc.set_threads(threads)
+        n, iters, t0 = 0, 0, time.perf_counter()
+        while True:
+            _, st, _ = orc.track_path(int(PrecisionMode.D), wd.g, wd.f, wd.gamma, wd.k, wd.start, wd.params)
+            n += 1
+            iters += st.newton_iters
+            if time.perf_counter() - t0 > seconds / 2:
+                break
+        dt = time.perf_counter() - t0
+        r = {"sec_per_path": dt / n, "sec_per_newton_iter": dt / max(1, iters), "cores": threads,
+             "paths": n, "newton_iters_per_path": iters / n, "workload": wd.name}
+        if best is None or r["sec_per_path"] < best["sec_per_path"]:
+            best = r
+    best["cores_available"] = os.cpu_count() or 1
+    return best
 
 
 def run_reference(args):

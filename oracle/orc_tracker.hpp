@@ -364,25 +364,39 @@ struct Tracker {
     std::vector<C> Rm((size_t)n * (n + 1));
     std::vector<R> inv(n);
     double maxnorm = 0.0;
+    bool ok = true;
+    // one parallel region per factorisation (a fork/join per column cost more
+    // than the columns of a 64 x 64 system): column k is normalised by one
+    // thread, the updates j > k are shared; every column's arithmetic is the
+    // same single-thread sequence, so the result does not depend on the team
+#pragma omp parallel if ((long)N * n >= 1024)
     for (int k = 0; k < n; ++k) {
       C* ak = &Amat[(size_t)k * N];
-      const R nrm2 = canon_sum<R>(N, P, [&](int i) { return A::norm_sqr(ak[i]); });
-      const R rkk = real_sqrt(nrm2);
-      const double d = A::to_double(rkk);
-      maxnorm = d > maxnorm ? d : maxnorm;
-      if (!(d > sqrt_eps * maxnorm)) return false;
-      inv[k] = R(1.0) / rkk;
-      for (int i = 0; i < N; ++i) ak[i] = ak[i] * inv[k];
-      Rm[(size_t)k * (n + 1) + k] = C(rkk, R(0.0));
-#pragma omp parallel for schedule(static)
+#pragma omp single
+      {
+        const R nrm2 = canon_sum<R>(N, P, [&](int i) { return A::norm_sqr(ak[i]); });
+        const R rkk = real_sqrt(nrm2);
+        const double d = A::to_double(rkk);
+        maxnorm = d > maxnorm ? d : maxnorm;
+        if (!(d > sqrt_eps * maxnorm)) {
+          ok = false;
+        } else {
+          inv[k] = R(1.0) / rkk;
+          for (int i = 0; i < N; ++i) ak[i] = ak[i] * inv[k];
+          Rm[(size_t)k * (n + 1) + k] = C(rkk, R(0.0));
+        }
+      }  // implicit barrier: ok, q_k and inv[k] visible to the team
+      if (!ok) break;
+#pragma omp for schedule(static)
       for (int j = k + 1; j <= n; ++j) {
         C* aj = &Amat[(size_t)j * N];
         const C rkj = canon_sum<C>(N, P, [&](int i) { return A::conj(ak[i]) * aj[i]; });
         Rm[(size_t)k * (n + 1) + j] = rkj;
         if (j < n || k < n - 1)
           for (int i = 0; i < N; ++i) aj[i] = aj[i] - rkj * ak[i];
-      }
+      }  // implicit barrier
     }
+    if (!ok) return false;
     dx.assign(n, C());
     for (int k = n - 1; k >= 0; --k) {
       C acc = Rm[(size_t)k * (n + 1) + n];
