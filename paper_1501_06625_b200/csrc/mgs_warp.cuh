@@ -524,12 +524,15 @@ __device__ __noinline__ double backsub_blocked(const DevPlan& P, const Work& W, 
     if (w == b) {  // diagonal block: the sequential chain
       const long long tb0 = clock64();
       // R column j is stored for every row 0..n-1 (entries below the diagonal
-      // are unused), so the prefetch needs no guard
-      cplx<R> cur = load_c<R>(Rs, SR, (long)jtop * n + i);
+      // are unused), so the prefetch needs no guard; the lanes past row n-1
+      // (n % 32 != 0) read row n-1 instead of running off the last plane
+      // (n < 16: past the staged copy) and never use the value
+      const int ir = min(i, n - 1);
+      cplx<R> cur = load_c<R>(Rs, SR, (long)jtop * n + ir);
 #pragma unroll 4
       for (int j = jtop; j >= j0; --j) {
         const int jl = j - j0;
-        const cplx<R> nxt = load_c<R>(Rs, SR, (long)(j > 0 ? j - 1 : 0) * n + i);
+        const cplx<R> nxt = load_c<R>(Rs, SR, (long)(j > 0 ? j - 1 : 0) * n + ir);
         const cplx<R> xs_l = c_scale(acc, inv);  // meaningful in lane jl: dx_j
         acc = pick(lane == jl, xs_l, acc);
         const cplx<R> xj = shfl0(xs_l, jl);

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 from conftest import assert_bits_equal
+import structured
 
 import paper_1501_06625_b200 as pt
 from paper_1501_06625_b200 import PolynomialSystem, PrecisionMode as PM, StepControlParams
@@ -195,3 +196,23 @@ def test_step_doubling_rule(oracle):
         else:
             succ = 0
             dt = dt / 2
+
+
+@pytest.mark.parametrize("n,prec,seed", structured.CASES,
+                         ids=lambda v: str(v) if not isinstance(v, PM) else v.name)
+def test_restatement_matches_reference_build_on_structured_systems(oracle, ref_oracle, n, prec, seed):
+    """The oracle the device is checked against (tests/test_gpu_random.py)
+    equals the reference-header build on the randomly structured systems too:
+    every path's stats, trace and end point, whatever the path's outcome."""
+    f, g, gamma, params, starts = structured.case(n, prec, seed, structured.max_steps(prec))
+    cap = params.max_steps + 2
+    for p in range(starts.shape[0]):
+        e1, s1, t1 = oracle.track_path(int(prec), g, f, gamma, 2, starts[p], params, cap)
+        e2, s2, t2 = ref_oracle.track_path(int(prec), g, f, gamma, 2, starts[p], params, cap)
+        assert (s1.status, s1.failure_kind, s1.steps, s1.accepted, s1.newton_iters) == (
+            s2.status, s2.failure_kind, s2.steps, s2.accepted, s2.newton_iters)
+        assert_bits_equal(np.array([s1.final_residual, s1.final_update, s1.t_end]),
+                          np.array([s2.final_residual, s2.final_update, s2.t_end]), "stats")
+        assert_bits_equal(np.array([(e.t, e.residual, e.update) for e in t1]).reshape(-1),
+                          np.array([(e.t, e.residual, e.update) for e in t2]).reshape(-1), "trace")
+        assert_bits_equal(e1, e2, f"end point of path {p}")
