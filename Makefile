@@ -8,9 +8,12 @@
 NVCC     ?= /usr/local/cuda/bin/nvcc
 HOSTCXX  := $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo g++)
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-# --fmad=false + explicit _rn intrinsics: no FMA contraction anywhere (bit parity)
+# --fmad=false + explicit _rn intrinsics: no FMA contraction anywhere (bit parity).
+# No --split-compile: its parallel optimisation is not deterministic (two
+# builds of the same sources gave different register / stack allocations and
+# single-path times 7-18 % apart); the TUs still compile in parallel (make -j).
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -ccbin $(HOSTCXX) \
-            -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills --split-compile=0 $(EXTRA_NVFLAGS)
+            -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills $(EXTRA_NVFLAGS)
 HOSTFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wno-unknown-pragmas
 PKG      := paper_1501_06625_b200
 SRC      := $(PKG)/csrc

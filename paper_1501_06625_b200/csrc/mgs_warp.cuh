@@ -524,15 +524,15 @@ __device__ __noinline__ double backsub_blocked(const DevPlan& P, const Work& W, 
     if (w == b) {  // diagonal block: the sequential chain
       const long long tb0 = clock64();
       // R column j is stored for every row 0..n-1 (entries below the diagonal
-      // are unused), so the prefetch needs no guard; the lanes past row n-1
-      // (n % 32 != 0) read row n-1 instead of running off the last plane
-      // (n < 16: past the staged copy) and never use the value
-      const int ir = min(i, n - 1);
-      cplx<R> cur = load_c<R>(Rs, SR, (long)jtop * n + ir);
+      // are unused), so the prefetch needs no guard; lanes past row n-1 read
+      // up to 31 - 2n doubles past the last plane, inside the tail padding of
+      // the staged copy (backsub_stage_doubles) or of the Rm / inv arrays
+      // (make_layout), and never use the value
+      cplx<R> cur = load_c<R>(Rs, SR, (long)jtop * n + i);
 #pragma unroll 4
       for (int j = jtop; j >= j0; --j) {
         const int jl = j - j0;
-        const cplx<R> nxt = load_c<R>(Rs, SR, (long)(j > 0 ? j - 1 : 0) * n + ir);
+        const cplx<R> nxt = load_c<R>(Rs, SR, (long)(j > 0 ? j - 1 : 0) * n + i);
         const cplx<R> xs_l = c_scale(acc, inv);  // meaningful in lane jl: dx_j
         acc = pick(lane == jl, xs_l, acc);
         const cplx<R> xj = shfl0(xs_l, jl);
@@ -557,9 +557,11 @@ __device__ __noinline__ double backsub_blocked(const DevPlan& P, const Work& W, 
   return block_nan_max(u, sh.red);
 }
 
-// doubles of CTA 0's shared-memory copy of R (2L planes of n(n+1)) and 1/r_kk
+// doubles of CTA 0's shared-memory copy of R (2L planes of n(n+1)) and 1/r_kk,
+// plus 32 doubles of tail padding for the unguarded prefetch of the lanes past
+// row n-1 in backsub_blocked (n < 16: up to 31 - 2n - Ln doubles past the copy)
 __host__ __device__ inline size_t backsub_stage_doubles(int L, int n) {
-  return (size_t)2 * L * n * (n + 1) + (size_t)L * n;
+  return (size_t)2 * L * n * (n + 1) + (size_t)L * n + 32;
 }
 
 // Back substitution of the warp MGS, run by CTA 0 after the MGS barrier: all

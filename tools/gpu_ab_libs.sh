@@ -10,3 +10,10 @@ for rep in 1 2; do
     done
   done
 done
+if [ -n "$BATCH" ]; then
+  for rep in 1 2; do for tag in ${TAGS:-base mono slots}; do
+    f=$O/${tag}_batch_$rep.json
+    PT_LIB_PATH=abprev/lib_$tag.so timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $f 2>&1
+    python -c "import json; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$tag batch $rep', round(d['value'],1), round(d['e2e']['value'],1))" 2>&1 | tail -1
+  done; done
+fi
