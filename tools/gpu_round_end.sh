@@ -1,6 +1,6 @@
 # end-of-round verification on one B200 (run through gpurun):
 #   every GPU test, smoke(), the default bench line, the reference arm, the single-path lines
-O=gpurun_out/r02end3; mkdir -p $O
+O=gpurun_out/r02end4; mkdir -p $O
 timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 timeout 1200 python bench.py > $O/bench_batch32_dd.json 2> $O/bench_batch32_dd.err
