@@ -173,10 +173,14 @@ size_t engine_smem(int L, int N, int n, int nblocks, bool cluster_or_block, int*
   }
   return *warp ? mgs_warp_bytes(L, N, n, nblocks, *warp == 2) : mgs_smem_bytes(L, N, n, nblocks);
 }
-int warp_mgs_block() {
+// Default block: 8 columns per CTA block in D (chandra-64 D 2.58 vs 2.63 ms
+// per path with 4), 4 in DD / QD (chandra-64 DD 11.84 vs 11.97 ms with 8;
+// deterministic build, same box, twice: DESIGN.md §5.1).
+int warp_mgs_block(int L) {
+  const int def = L == 1 ? 8 : 4;
   const char* e = getenv("PT_MGS_B");
-  const int b = e ? atoi(e) : 4;
-  return (b == 1 || b == 2 || b == 4 || b == 8) ? b : 4;
+  const int b = e ? atoi(e) : def;
+  return (b == 1 || b == 2 || b == 4 || b == 8) ? b : def;
 }
 
 int set_dyn_smem(const void* fn, size_t bytes) {
@@ -448,7 +452,7 @@ int pt_plan_create(int device, pt_prec prec, const pt_system_desc* g, const pt_s
     while (dp.mono_long < p->M && hp.mono_size[dp.mono_long] >= split) ++dp.mono_long;
     dp.P_mgs = ptplan::width_mgs(hp.N);
     dp.mgs_gw = ptplan::mgs_group_warps(hp.N);
-    dp.mgs_B = warp_mgs_block();
+    dp.mgs_B = warp_mgs_block(p->L);
     dp.mono_size = (const int32_t*)(base + offs[0]);
     dp.mono_vbeg = (const int32_t*)(base + offs[1]);
     dp.mono_out = (const int32_t*)(base + offs[2]);
